@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: full-graph multi-head sparse graph attention, forward + backward
+(Eq. 2/4/5 and Section 2.2), on a products-shaped synthetic graph
+(BASELINE.json configs[2]: 2,449,029 nodes, 123,718,280 stored entries,
+4 heads x 64, bf16).
+
+One step = gt_attn_fwd + gt_attn_bwd over the whole graph (all of SURVEY 8(a) rows a4-a8 that apply
+at this world size).  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse-attn fwd+bwd edges/s/GPU at 1/2/4/8 B200; % HBM roofline; speedup"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--strategy", default=None, help="auto|allgather|halo (world > 1)")
+    ap.add_argument("--heavy", type=int, default=0, help="heavy row/column threshold (0 = library default)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-edges", type=int, default=0, help="0 = auto-size (~15 s of oracle work)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def alg_bytes(h, d, elt):
+    """SURVEY.md 8(d) no-reuse gather model: algorithmic bytes per edge and per row of each pass.
+    I = 4 B column/row index, R = 4 B row offset, D = h*d, b = dtype bytes."""
+    D, I, R = h * d, 4, 4
+    return {
+        "fwd": (I + 2 * D * elt, R + 2 * D * elt + 4 * h),          # k_j, v_j | q in, y out, lse out
+        "bwd_rows": (I + 2 * D * elt, R + 3 * D * elt + 8 * h),     # k_j, v_j | q, dy in, dq out, lse in, D out
+        "bwd_cols": (I + 2 * D * elt + 8 * h, R + 4 * D * elt),     # q_i, dy_i, lse_i, D_i | k, v in, dk, dv out
+    }
+
+
+class Clocks:
+    """Samples nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = str(gpu_index)
+        self.proc = None
+        self.out = ""
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", self.idx, "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def induced_prefix_subgraph(rp, ci, target_edges):
+    """CPU-baseline sample: the subgraph induced by the first R nodes (R chosen so it holds about
+    target_edges entries).  Keeps the generator's locality/community structure."""
+    import numpy as np
+    n = len(rp) - 1
+    R = int(np.searchsorted(rp, target_edges * 1.12))
+    R = max(1, min(n, R))
+    rows = []
+    cols = ci[:rp[R]]
+    rid = np.repeat(np.arange(R, dtype=np.int64), np.diff(rp[:R + 1]))
+    keep = cols < R
+    sub_rp = np.zeros(R + 1, np.int64)
+    np.add.at(sub_rp, rid[keep] + 1, 1)
+    sub_rp = np.cumsum(sub_rp)
+    del rows
+    return sub_rp, cols[keep].astype(np.int32), R
+
+
+def oracle_step(sub_rp, sub_ci, R, cfg, seed, scale):
+    import gtgen
+    import oracle
+    q, k, v, dy = (gtgen.features(seed, nm, R, cfg.heads, cfg.d, cfg.dtype) for nm in ("q", "k", "v", "dy"))
+    t0 = time.perf_counter()
+    oracle.forward(sub_rp, sub_ci, q, k, v, scale)
+    oracle.backward(sub_rp, sub_ci, q, k, v, dy, scale)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_size(rp, ci, cfg, scale, budget_s):
+    """Calibrates the oracle sample so one fwd+bwd run takes about budget_s seconds."""
+    sub_rp, sub_ci, R = induced_prefix_subgraph(rp, ci, 200_000)
+    t = oracle_step(sub_rp, sub_ci, R, cfg, 7, scale)
+    rate = max(1.0, sub_rp[-1] / max(t, 1e-6))
+    return int(min(len(ci), max(200_000, rate * budget_s)))
+
+
+def run_reference(args):
+    """--impl reference: the oracle (oracle/, fp64 C, all host cores) timed as it stands on a bounded
+    sample of the same workload; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import gtgen
+    cfg = gtgen.CONFIGS[args.config]
+    rp, ci = gtgen.make_graph(cfg.graph)
+    scale = 1.0 / math.sqrt(cfg.heads * cfg.d)
+    target = args.cpu_sample_edges or cpu_sample_size(rp, ci, cfg, scale, budget_s=3.0)
+    sub_rp, sub_ci, R = induced_prefix_subgraph(rp, ci, target)
+    for _ in range(args.warmup):
+        oracle_step(sub_rp, sub_ci, R, cfg, 9, scale)
+    t = 0.0
+    for _ in range(args.steps):
+        t += oracle_step(sub_rp, sub_ci, R, cfg, 9, scale)
+    ms = t / args.steps * 1e3
+    val = float(sub_rp[-1]) / (ms / 1e3)
+    cores = gtgen.num_threads()
+    sample = (f"subgraph induced by the first {R} of {len(rp) - 1} nodes ({int(sub_rp[-1])} of {len(ci)} entries), "
+              f"fp64 oracle fwd+bwd per step")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "edges/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} (oracle sample)", "nodes": len(rp) - 1, "nnz": int(len(ci)),
+                       "heads": cfg.heads, "head_dim": cfg.d, "input_dtype": cfg.dtype},
+            "cpu_baseline": {"value": val, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gtgen
+    import paper_2604_16715_b200 as gt
+    from paper_2604_16715_b200 import _build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    cfg = gtgen.CONFIGS[args.config]
+    h, d = cfg.heads, cfg.d
+    elt = 4 if cfg.dtype == "f32" else 2
+    scale = 1.0 / math.sqrt(h * d)
+
+    t_gen = time.perf_counter()
+    rp, ci = gtgen.make_graph(cfg.graph)
+    n, nnz = len(rp) - 1, len(ci)
+    t_gen = time.perf_counter() - t_gen
+
+    comm = gt.NcclComm() if world > 1 else None
+    strategy = args.strategy or ("single" if world == 1 else "auto")
+    t_plan = time.perf_counter()
+    plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
+                   strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local)
+    torch.cuda.synchronize()
+    t_plan = time.perf_counter() - t_plan
+    info = plan.info()
+    lo, hi = plan.row_lo, plan.row_hi
+
+    def feat(nm):
+        x = gtgen.features(1234, nm, n, h, d, cfg.dtype, row_lo=lo, row_hi=hi)
+        t = torch.from_numpy(x.view(np.int16) if x.dtype == np.uint16 else x)
+        t = t.view(torch.bfloat16) if cfg.dtype == "bf16" else t
+        return t.contiguous()
+
+    host = {nm: feat(nm) for nm in ("q", "k", "v", "dy")}
+    dev = {nm: t.cuda() for nm, t in host.items()}
+    q, k, v, dy = dev["q"], dev["k"], dev["v"], dev["dy"]
+    y = torch.empty_like(q)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    lse = torch.empty((hi - lo, h), dtype=torch.float32, device=q.device)
+
+    def step():
+        plan.fwd(q, k, v, y, lse)
+        plan.bwd(q, k, v, lse, dy, dq, dk, dv)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    plan.timings()  # reset the stage sums: only the timed region is reported
+    clocks = Clocks(local)
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = plan.timings()
+    clk = clocks.stop() if rank == 0 else None
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=q.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- roofline of the dominant kernel stage (per launch, device-timed on the launching stream) ----
+    per = alg_bytes(h, d, elt)
+    units = {"fwd": (info["nnz_local"], info["n_local"]), "bwd_rows": (info["nnz_local"], info["n_local"]),
+             "bwd_cols": (info["nnz_in_local"], info["n_local"])}
+    stage_ms = {s: (stages[s][0] / max(stages[s][1], 1)) for s in ("fwd", "bwd_rows", "bwd_cols")}
+    dom = max(stage_ms, key=stage_ms.get)
+    dom_bytes = per[dom][0] * units[dom][0] + per[dom][1] * units[dom][1]
+    peak, peak_src = peaks()
+    achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
+    step_bytes = sum(per[s][0] * units[s][0] + per[s][1] * units[s][1] for s in per)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(cfg.name, {}).get(dom)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "alg_bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]}
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pin = {nm: t.pin_memory() for nm, t in host.items()}
+        outs = [torch.empty_like(pin["q"]).pin_memory() for _ in range(4)]
+        plse = torch.empty((hi - lo, h), dtype=torch.float32).pin_memory()
+        plan.fwd_bwd_host(pin["q"], pin["k"], pin["v"], pin["dy"], outs[0], plse, outs[1], outs[2], outs[3])
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.fwd_bwd_host(pin["q"], pin["k"], pin["v"], pin["dy"], outs[0], plse, outs[1], outs[2], outs[3])
+        te = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([te], dtype=torch.float64, device=q.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        tb = (hi - lo) * h * d * elt
+        e2e = {"value": nnz / te, "unit": "edges/s", "h2d_bytes_per_step": 4 * tb,
+               "d2h_bytes_per_step": 4 * tb + (hi - lo) * h * 4, "ms_per_step": te * 1e3}
+        plan.timings()
+
+    # ---- CPU baseline: the oracle as it stands, bounded sample, rank 0 at N=1 only ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        target = args.cpu_sample_edges or cpu_sample_size(rp, ci, cfg, scale, budget_s=15.0)
+        sub_rp, sub_ci, R = induced_prefix_subgraph(rp, ci, target)
+        tc = oracle_step(sub_rp, sub_ci, R, cfg, 9, scale)
+        cpu = {"value": float(sub_rp[-1]) / tc, "unit": "edges/s", "cores": gtgen.num_threads(), "kind": "oracle",
+               "sample": f"fp64 oracle fwd+bwd on the subgraph induced by the first {R} nodes "
+                         f"({int(sub_rp[-1])} entries), {tc:.1f} s"}
+
+    if rank == 0:
+        value = nnz / (ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "config": {"workload": cfg.name, "nodes": n, "nnz": nnz, "heads": h, "head_dim": d,
+                       "strategy": info["strategy_name"], "parallelism": f"graph-row x{world}",
+                       "l2": "inputs larger than L2 (K, V tables 1.25 GB each vs 126 MB L2); no flush",
+                       "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 1024},
+            "roofline": roofline,
+            "step_hbm_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
+            "stages_ms": {s: stages[s][0] / max(stages[s][1], 1) for s in stages},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": (info["launches_fwd"] + info["launches_bwd"]) * args.steps,
+            "clocks": clk,
+            "plan": {"t_gen_s": t_gen, "t_plan_s": t_plan, "heavy_rows": info["heavy_rows"],
+                     "heavy_cols": info["heavy_cols"], "exch_fwd_bytes": info["exch_fwd_bytes"],
+                     "exch_bwd_bytes": info["exch_bwd_bytes"], "predicted_ms": info["predicted_ms"]},
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -52,6 +52,8 @@ def _load():
                                    ctypes.POINTER(ctypes.c_void_p)]
         _lib.gen_free.argtypes = [ctypes.c_void_p]
         _lib.gen_normal_f32.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64, ctypes.c_void_p]
+        _lib.gen_normal_f32_range.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_void_p]
         _lib.gen_f32_to_bf16.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
         _lib.gen_num_threads.restype = ctypes.c_int
     return _lib
@@ -190,6 +192,16 @@ def normal_f32(seed: int, tensor_id: int, shape) -> np.ndarray:
     return out.reshape(shape)
 
 
+def normal_f32_rows(seed: int, tensor_id: int, row_lo: int, row_hi: int, row_elems: int) -> np.ndarray:
+    """Rows [row_lo, row_hi) of the [n, row_elems] tensor normal_f32(seed, tensor_id, (n, row_elems))."""
+    lib = _load()
+    n = (row_hi - row_lo) * row_elems
+    out = np.empty(n, np.float32)
+    if n:
+        lib.gen_normal_f32_range(ctypes.c_uint64(seed), tensor_id, row_lo * row_elems, n, out.ctypes.data)
+    return out.reshape(row_hi - row_lo, row_elems)
+
+
 def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even fp32 -> bf16, returned as uint16 bit patterns."""
     lib = _load()
@@ -204,9 +216,12 @@ def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
-def features(seed: int, name: str, n: int, heads: int, d: int, dtype: str, scale: float = 1.0):
-    """Feature tensor [n, heads, d]: fp32 array, or uint16 bf16 bits when dtype == 'bf16'."""
-    x = normal_f32(seed, TENSOR_IDS[name], (n, heads, d))
+def features(seed: int, name: str, n: int, heads: int, d: int, dtype: str, scale: float = 1.0,
+             row_lo: int = 0, row_hi: int | None = None):
+    """Feature tensor rows [row_lo, row_hi) of [n, heads, d]: fp32 array, or uint16 bf16 bits when
+    dtype == 'bf16'.  Any row slice equals the same rows of the full tensor."""
+    row_hi = n if row_hi is None else row_hi
+    x = normal_f32_rows(seed, TENSOR_IDS[name], row_lo, row_hi, heads * d).reshape(row_hi - row_lo, heads, d)
     if scale != 1.0:
         x = (x * np.float32(scale)).astype(np.float32)
     if dtype == "bf16":

@@ -67,23 +67,25 @@ static inline uint64_t mix64(uint64_t z) {
 }
 
 /* -------------------------------------------------------------- features -- */
-/* i.i.d. N(0,1) via Box-Muller; counter = flat index / 4, stream = tensor_id. */
-void gen_normal_f32(uint64_t seed, uint32_t tensor_id, int64_t n, float* out) {
+/* i.i.d. N(0,1) via Box-Muller; element i of tensor `tensor_id` comes from Philox counter i / 4,
+ * so any slice [start, start + n) of the flat tensor can be generated on its own. */
+static inline float normal_at(uint64_t seed, uint32_t tensor_id, int64_t i) {
+  uint32_t r[4];
+  rng4(seed, 0x10000u + tensor_id, (uint64_t)(i >> 2), r);
+  int c = (int)(i & 3);
+  double u1 = ((double)(r[c < 2 ? 0 : 2] >> 8) + 0.5) * (1.0 / 16777216.0);
+  double u2 = ((double)(r[c < 2 ? 1 : 3] >> 8) + 0.5) * (1.0 / 16777216.0);
+  double rad = sqrt(-2.0 * log(u1)), th = 6.283185307179586 * u2;
+  return (float)((c & 1) ? rad * sin(th) : rad * cos(th));
+}
+
+void gen_normal_f32_range(uint64_t seed, uint32_t tensor_id, int64_t start, int64_t n, float* out) {
 #pragma omp parallel for schedule(static)
-  for (int64_t g = 0; g < (n + 3) / 4; ++g) {
-    uint32_t r[4];
-    rng4(seed, 0x10000u + tensor_id, (uint64_t)g, r);
-    double u1 = ((double)(r[0] >> 8) + 0.5) * (1.0 / 16777216.0);
-    double u2 = ((double)(r[1] >> 8) + 0.5) * (1.0 / 16777216.0);
-    double u3 = ((double)(r[2] >> 8) + 0.5) * (1.0 / 16777216.0);
-    double u4 = ((double)(r[3] >> 8) + 0.5) * (1.0 / 16777216.0);
-    double ra = sqrt(-2.0 * log(u1)), rb = sqrt(-2.0 * log(u3));
-    double ta = 6.283185307179586 * u2, tb = 6.283185307179586 * u4;
-    float v[4] = {(float)(ra * cos(ta)), (float)(ra * sin(ta)), (float)(rb * cos(tb)),
-                  (float)(rb * sin(tb))};
-    for (int k = 0; k < 4; ++k)
-      if (4 * g + k < n) out[4 * g + k] = v[k];
-  }
+  for (int64_t i = 0; i < n; ++i) out[i] = normal_at(seed, tensor_id, start + i);
+}
+
+void gen_normal_f32(uint64_t seed, uint32_t tensor_id, int64_t n, float* out) {
+  gen_normal_f32_range(seed, tensor_id, 0, n, out);
 }
 
 /* fp32 -> bf16 bits, round to nearest even (inputs are finite). */

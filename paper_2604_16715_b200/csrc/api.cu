@@ -1,0 +1,647 @@
+// C ABI entry points of libgt.so (include/gt.h): plan construction, forward, backward, exports.
+#include <cuda_runtime.h>
+#include <omp.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "gt_internal.h"
+
+namespace gt {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+gt_status fail(gt_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+gt_status DevBuf::alloc(size_t n) {
+  release();
+  if (n == 0) return GT_OK;
+  cudaError_t e = cudaMalloc(&p, n);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? GT_ENOMEM : GT_ECUDA,
+                std::string("cudaMalloc(") + std::to_string(n) + "): " + cudaGetErrorString(e));
+  }
+  bytes = n;
+  return GT_OK;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+template <typename V>
+static gt_status upload(DevBuf& b, const V* src, size_t count) {
+  GT_TRY(b.alloc(std::max<size_t>(count, 1) * sizeof(V)));
+  if (count) GT_CUDA_TRY(cudaMemcpy(b.p, src, count * sizeof(V), cudaMemcpyHostToDevice));
+  return GT_OK;
+}
+
+static gt_status upload_chunks(ChunkTable& t) {
+  if (t.nchunks() == 0) return GT_OK;
+  GT_TRY(upload(t.d_ids, t.ids.data(), t.ids.size()));
+  GT_TRY(upload(t.d_first, t.first.data(), t.first.size()));
+  GT_TRY(upload(t.d_lo, t.chunk_lo.data(), t.chunk_lo.size()));
+  GT_TRY(upload(t.d_hi, t.chunk_hi.data(), t.chunk_hi.size()));
+  GT_TRY(upload(t.d_owner, t.chunk_owner.data(), t.chunk_owner.size()));
+  return GT_OK;
+}
+
+static int owner_of(const std::vector<int64_t>& bounds, int64_t j) {
+  // last r with bounds[r] <= j among non-empty ranges
+  int r = (int)(std::upper_bound(bounds.begin(), bounds.end(), j) - bounds.begin()) - 1;
+  return r;
+}
+
+// Remaps a global id to this rank's gathered-row index space: owned -> id - lo;
+// remote -> n_local + slot in the receive table (halo: position in the sorted halo list;
+// all-gather: owner * n_max + offset within the owner's block).
+static void remap_ids(int32_t* ids, int64_t count, const gt_plan_s* P, const std::vector<int32_t>& halo, bool ag) {
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < count; ++e) {
+    int64_t j = ids[e];
+    int64_t out;
+    if (j >= P->lo && j < P->hi) {
+      out = j - P->lo;
+    } else if (ag) {
+      int o = owner_of(P->bounds, j);
+      out = P->n_local + (int64_t)o * P->n_max + (j - P->bounds[o]);
+    } else {
+      out = P->n_local + (std::lower_bound(halo.begin(), halo.end(), (int32_t)j) - halo.begin());
+    }
+    ids[e] = (int32_t)out;
+  }
+}
+
+// rows of `ids` (ascending global ids) grouped by owner: offsets/counts per rank
+static void group_by_owner(const std::vector<int32_t>& ids, const std::vector<int64_t>& bounds,
+                           std::vector<int64_t>& off, std::vector<int64_t>& cnt) {
+  const int w = (int)bounds.size() - 1;
+  off.assign(w, 0);
+  cnt.assign(w, 0);
+  for (int s = 0; s < w; ++s) {
+    auto a = std::lower_bound(ids.begin(), ids.end(), (int32_t)bounds[s]);
+    auto b = std::lower_bound(ids.begin(), ids.end(), (int32_t)bounds[s + 1]);
+    off[s] = a - ids.begin();
+    cnt[s] = b - a;
+  }
+}
+
+struct Pattern {  // one exchange: rows to send per peer (local ids) and rows to receive per peer
+  std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
+  std::vector<int32_t> send_idx;  // local ids, concatenated in peer order
+  int64_t recv_rows = 0;
+};
+
+static void make_halo_pattern(const gt_plan_s* P, const std::vector<std::vector<int32_t>>& send,
+                              const std::vector<int32_t>& recv_ids, Pattern& pt) {
+  const int w = P->world;
+  pt.send_off.assign(w, 0);
+  pt.send_cnt.assign(w, 0);
+  pt.send_idx.clear();
+  for (int s = 0; s < w; ++s) {
+    pt.send_off[s] = (int64_t)pt.send_idx.size();
+    pt.send_cnt[s] = (int64_t)send[s].size();
+    for (int32_t j : send[s]) pt.send_idx.push_back((int32_t)(j - P->lo));
+  }
+  group_by_owner(recv_ids, P->bounds, pt.recv_off, pt.recv_cnt);
+  pt.recv_rows = (int64_t)recv_ids.size();
+}
+
+static void make_ag_pattern(const gt_plan_s* P, Pattern& pt) {
+  const int w = P->world;
+  pt.send_off.assign(w, 0);
+  pt.send_cnt.assign(w, P->n_max);
+  pt.recv_off.resize(w);
+  pt.recv_cnt.assign(w, P->n_max);
+  for (int s = 0; s < w; ++s) pt.recv_off[s] = (int64_t)s * P->n_max;
+  pt.recv_cnt[P->rank] = 0;
+  pt.send_idx.resize(P->n_local);
+  std::iota(pt.send_idx.begin(), pt.send_idx.end(), 0);
+  pt.recv_rows = (int64_t)w * P->n_max;
+}
+
+static int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
+
+}  // namespace gt
+
+using namespace gt;
+
+cudaEvent_t gt_plan_s::take_event() {
+  if (!ev_pool.empty()) {
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void gt_plan_s::mark_begin(int, cudaStream_t st, cudaEvent_t* a) {
+  *a = nullptr;
+  if (!profile) return;
+  *a = take_event();
+  cudaEventRecord(*a, st);
+}
+void gt_plan_s::mark_end(int stage, cudaStream_t st, cudaEvent_t a) {
+  if (!profile || !a) return;
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, st);
+  recs.push_back({stage, a, b});
+}
+
+gt_plan_s::~gt_plan_s() {
+  for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (side) cudaStreamDestroy(side);
+  if (comm && own_comm) delete comm;
+}
+
+extern "C" {
+
+const char* gt_last_error(void) { return g_err.c_str(); }
+
+const char* gt_version(void) {
+  return "libgt 0.1 (sm_100a; fused SDDMM+softmax+SpMM fwd, row/column backward; NCCL/loopback exchange)";
+}
+
+void gt_default_opts(gt_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->dtype = GT_BF16;
+  o->strategy = GT_AUTO;
+  o->validate = 1;
+  o->device = -1;
+}
+
+static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads, int d, int world,
+                           const gt_opts* opts, gt_plan_t* out) {
+  if (!csr || !out || !opts) return fail(GT_EINVAL, "gt_plan: null argument");
+  *out = nullptr;
+  if (n < 0 || nnz < 0 || n >= (1ll << 31) - 1 || nnz >= (1ll << 31) - 1)
+    return fail(GT_EINVAL, "gt_plan: n and nnz must be in [0, 2^31 - 1)");
+  if (!csr->row_ptr || (nnz > 0 && !csr->col_idx)) return fail(GT_EINVAL, "gt_plan: null CSR arrays");
+  if (heads <= 0 || d <= 0) return fail(GT_EINVAL, "gt_plan: heads and d must be positive");
+  if (!shape_supported(heads, d, opts->dtype))
+    return fail(GT_ECONFIG, "gt_plan: unsupported shape: need heads in {1,2,4,8}, heads*d in {128,256,512}, "
+                            "dtype f32|bf16; got heads=" + std::to_string(heads) + " d=" + std::to_string(d));
+  if (world < 1 || opts->rank < 0 || opts->rank >= world) return fail(GT_EINVAL, "gt_plan: bad world/rank");
+  if (world > 1 && (!opts->comm || (opts->comm_kind != GT_COMM_NCCL && opts->comm_kind != GT_COMM_LOOPBACK)))
+    return fail(GT_EINVAL, "gt_plan: world > 1 needs a communicator");
+  if (world == 1 && (opts->strategy == GT_ALLGATHER || opts->strategy == GT_HALO))
+    return fail(GT_ECONFIG, "gt_plan: multi-GPU strategy requested with world == 1");
+  if (opts->partition != 0 && opts->partition != 1) return fail(GT_EINVAL, "gt_plan: partition must be 0 or 1");
+  if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
+  if (opts->validate) GT_TRY(validate_csr(csr->row_ptr, csr->col_idx, n, nnz));
+  else if (csr->row_ptr[n] != nnz) return fail(GT_EGRAPH, "row_ptr[n] != nnz");
+
+  if (opts->device >= 0) GT_CUDA_TRY(cudaSetDevice(opts->device));
+  auto P = std::make_unique<gt_plan_s>();
+  GT_CUDA_TRY(cudaGetDevice(&P->device));
+  GT_CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+  cudaStream_t st = P->side;
+  P->world = world;
+  P->rank = opts->rank;
+  P->heads = heads;
+  P->d = d;
+  P->dtype = opts->dtype;
+  P->n = n;
+  P->nnz = nnz;
+  P->scale = opts->scale > 0.f ? opts->scale : (float)(1.0 / std::sqrt((double)heads * d));
+  P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 1024;
+  P->profile = opts->profile != 0;
+  const int64_t D = (int64_t)heads * d;
+  const int elt = opts->dtype == GT_F32 ? 4 : 2;
+  P->kv_row_bytes = 2 * D * elt;
+  P->in_row_bytes = round16(2 * D * elt + 8 * heads);
+
+  gt_status cst = GT_OK;
+  if (world > 1) {
+    P->comm = opts->comm_kind == GT_COMM_NCCL ? make_nccl_comm(opts->comm, world, opts->rank, &cst)
+                                               : make_loopback_comm((gt_loopback_t)opts->comm, world, opts->rank, &cst);
+    if (!P->comm) return cst;
+  }
+
+  // ---- partition (reading Z9) ----
+  P->bounds.resize(world + 1);
+  partition_rows(n, csr->row_ptr, world, opts->partition, P->bounds.data());
+  P->lo = P->bounds[P->rank];
+  P->hi = P->bounds[P->rank + 1];
+  P->n_local = P->hi - P->lo;
+  P->nnz_local = csr->row_ptr[P->hi] - csr->row_ptr[P->lo];
+  for (int r = 0; r < world; ++r) P->n_max = std::max(P->n_max, P->bounds[r + 1] - P->bounds[r]);
+
+  // ---- full graph on device, A^T (CSC) ----
+  DevBuf full_rp, full_col_tmp, full_cp, full_row;
+  GT_TRY(upload(full_rp, csr->row_ptr, (size_t)n + 1));
+  const bool single = world == 1;
+  DevBuf* full_col = single ? &P->d_col : &full_col_tmp;
+  GT_TRY(upload(*full_col, csr->col_idx, (size_t)nnz));
+  DevBuf* cp = single ? &P->d_col_ptr : &full_cp;
+  DevBuf* rw = single ? &P->d_row : &full_row;
+  GT_TRY(cp->alloc(((size_t)n + 1) * sizeof(int64_t)));
+  GT_TRY(rw->alloc(std::max<size_t>((size_t)nnz, 1) * sizeof(int32_t)));
+  GT_TRY(build_csc_device(full_rp.as<int64_t>(), full_col->as<int32_t>(), n, nnz, cp->as<int64_t>(),
+                          rw->as<int32_t>(), st));
+  std::vector<int64_t> col_ptr_full((size_t)n + 1);
+  GT_CUDA_TRY(cudaMemcpy(col_ptr_full.data(), cp->p, ((size_t)n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+
+  // ---- local row slice (row pass) ----
+  std::vector<int64_t> rp_local((size_t)P->n_local + 1);
+  for (int64_t i = 0; i <= P->n_local; ++i) rp_local[i] = csr->row_ptr[P->lo + i] - csr->row_ptr[P->lo];
+  GT_TRY(upload(P->d_row_ptr, rp_local.data(), rp_local.size()));
+  // ---- local column slice (column pass) ----
+  const int64_t c0 = col_ptr_full[P->lo], c1 = col_ptr_full[P->hi];
+  P->nnz_in_local = c1 - c0;
+  P->h_col_ptr.resize((size_t)P->n_local + 1);
+  for (int64_t j = 0; j <= P->n_local; ++j) P->h_col_ptr[j] = col_ptr_full[P->lo + j] - c0;
+
+  // ---- multi-rank: halo sets, send lists, strategy ----
+  Pattern pf_halo, pb_halo, pf_ag, pb_ag;
+  if (!single) {
+    const int w = world;
+    const int64_t lo = P->lo, hi = P->hi;
+    const int64_t* rp = csr->row_ptr;
+    const int32_t* ci = csr->col_idx;
+    P->halo_out = halo_set(n, rp, ci, lo, hi, false);
+    P->halo_in = halo_set(n, rp, ci, lo, hi, true);
+    P->send_out.assign(w, {});
+    P->send_in.assign(w, {});
+    for (int s = 0; s < w; ++s) {
+      if (s == P->rank) continue;
+      P->send_out[s] = send_set(n, rp, ci, lo, hi, P->bounds[s], P->bounds[s + 1], false);
+      P->send_in[s] = send_set(n, rp, ci, lo, hi, P->bounds[s], P->bounds[s + 1], true);
+    }
+    make_halo_pattern(P.get(), P->send_out, P->halo_out, pf_halo);
+    make_halo_pattern(P.get(), P->send_in, P->halo_in, pb_halo);
+    make_ag_pattern(P.get(), pf_ag);
+    make_ag_pattern(P.get(), pb_ag);
+
+    int strategy = opts->strategy;
+    // cost model (Eq. 6-8 generalised): t_c = alpha (E_r + N_r) + t_exchange,c
+    const double alpha = 3200.0 / (0.6 * 6.45e12);  // s per (edge + row): gather-model bytes / 60% HBM
+    double units = (double)(P->nnz_local + P->nnz_in_local) / 2 + (double)P->n_local;
+    double t_compute = alpha * units;
+    GT_TRY(P->comm->max_host(&t_compute, st));
+    const double t_iter1 = alpha * (double)(nnz + n);
+    P->info.alpha_s_per_unit = alpha;
+    size_t free_b = 0, total_b = 0;
+    GT_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    for (int c : {(int)GT_ALLGATHER, (int)GT_HALO}) {
+      const Pattern& f = c == GT_ALLGATHER ? pf_ag : pf_halo;
+      const Pattern& b = c == GT_ALLGATHER ? pb_ag : pb_halo;
+      int64_t need = f.recv_rows * P->kv_row_bytes + b.recv_rows * P->in_row_bytes +
+                     std::max((int64_t)f.send_idx.size() * P->kv_row_bytes, (int64_t)b.send_idx.size() * P->in_row_bytes) +
+                     (c == GT_ALLGATHER ? P->n_max * (P->kv_row_bytes + P->in_row_bytes) : 0);
+      double fits = (double)need < 0.85 * (double)free_b ? 1.0 : 0.0;
+      double t_ex = INFINITY;
+      if (strategy == GT_AUTO && fits > 0) {
+        // measure the forward and backward exchanges of this pattern (2 warm-up + 3 timed)
+        DevBuf sb, rf, rb;
+        int64_t sbytes = std::max({(int64_t)f.send_idx.size() * P->kv_row_bytes,
+                                   (int64_t)b.send_idx.size() * P->in_row_bytes,
+                                   c == GT_ALLGATHER ? P->n_max * P->in_row_bytes : 0, (int64_t)16});
+        GT_TRY(sb.alloc((size_t)sbytes));
+        GT_TRY(rf.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
+        GT_TRY(rb.alloc((size_t)std::max<int64_t>(b.recv_rows * P->in_row_bytes, 16)));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float ms_best = 1e30f;
+        for (int it = 0; it < 5; ++it) {
+          GT_TRY(P->comm->barrier(st));
+          cudaEventRecord(e0, st);
+          if (c == GT_ALLGATHER) {
+            GT_TRY(P->comm->all_gather(sb.p, rf.p, P->n_max, P->kv_row_bytes, st));
+            GT_TRY(P->comm->all_gather(sb.p, rb.p, P->n_max, P->in_row_bytes, st));
+          } else {
+            GT_TRY(P->comm->exchange(sb.p, f.send_off.data(), f.send_cnt.data(), rf.p, f.recv_off.data(),
+                                     f.recv_cnt.data(), P->kv_row_bytes, st));
+            GT_TRY(P->comm->exchange(sb.p, b.send_off.data(), b.send_cnt.data(), rb.p, b.recv_off.data(),
+                                     b.recv_cnt.data(), P->in_row_bytes, st));
+          }
+          cudaEventRecord(e1, st);
+          GT_CUDA_TRY(cudaEventSynchronize(e1));
+          float ms = 0;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (it >= 2) ms_best = std::min(ms_best, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        t_ex = ms_best * 1e-3;
+        GT_TRY(P->comm->max_host(&t_ex, st));
+      }
+      double rows = (double)(f.recv_rows + b.recv_rows);
+      P->info.beta_s_per_row[c] = std::isfinite(t_ex) && rows > 0 ? t_ex / rows : 0.0;
+      P->info.predicted_ms[c] = std::isfinite(t_ex) ? (t_compute + t_ex) * 1e3 : INFINITY;
+      // Eq. 14 with beta_c * N replaced by the measured exchange time: p t_comm / (p - 1) <= t_iter(1)
+      P->info.agp_score[c] = std::isfinite(t_ex) ? world * t_ex / (world - 1) * 1e3 : INFINITY;
+      P->info.agp_feasible[c] = std::isfinite(t_ex) && world * t_ex / (world - 1) <= t_iter1;
+      if (!fits && strategy == c) return fail(GT_ENOMEM, "gt_plan: strategy buffers do not fit in device memory");
+    }
+    P->info.predicted_ms[GT_SINGLE] = t_iter1 * 1e3;
+    if (strategy == GT_AUTO) {
+      int32_t pick = P->info.predicted_ms[GT_HALO] < P->info.predicted_ms[GT_ALLGATHER] ? GT_HALO : GT_ALLGATHER;
+      GT_TRY(P->comm->broadcast_host(&pick, sizeof(pick), st));  // rank 0 decides
+      strategy = pick;
+    }
+    P->strategy = strategy;
+  } else {
+    P->strategy = GT_SINGLE;
+  }
+
+  // ---- remapped local CSR columns and CSC rows ----
+  if (!single) {
+    const bool ag = P->strategy == GT_ALLGATHER;
+    std::vector<int32_t> cols(csr->col_idx + csr->row_ptr[P->lo], csr->col_idx + csr->row_ptr[P->hi]);
+    remap_ids(cols.data(), (int64_t)cols.size(), P.get(), P->halo_out, ag);
+    GT_TRY(upload(P->d_col, cols.data(), cols.size()));
+    std::vector<int32_t> rows((size_t)P->nnz_in_local);
+    if (P->nnz_in_local)
+      GT_CUDA_TRY(cudaMemcpy(rows.data(), full_row.as<int32_t>() + c0, rows.size() * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost));
+    remap_ids(rows.data(), (int64_t)rows.size(), P.get(), P->halo_in, ag);
+    GT_TRY(upload(P->d_row, rows.data(), rows.size()));
+    GT_TRY(upload(P->d_col_ptr, P->h_col_ptr.data(), P->h_col_ptr.size()));
+    const Pattern& f = ag ? pf_ag : pf_halo;
+    const Pattern& b = ag ? pb_ag : pb_halo;
+    P->so_off = f.send_off; P->so_cnt = f.send_cnt; P->ro_off = f.recv_off; P->ro_cnt = f.recv_cnt;
+    P->si_off = b.send_off; P->si_cnt = b.send_cnt; P->ri_off = b.recv_off; P->ri_cnt = b.recv_cnt;
+    P->halo_out_rows = f.recv_rows;
+    P->halo_in_rows = b.recv_rows;
+    P->n_send_out = (int64_t)f.send_idx.size();
+    P->n_send_in = (int64_t)b.send_idx.size();
+    GT_TRY(upload(P->d_send_out_idx, f.send_idx.data(), f.send_idx.size()));
+    GT_TRY(upload(P->d_send_in_idx, b.send_idx.data(), b.send_idx.size()));
+    int64_t sbytes = std::max((int64_t)f.send_idx.size() * P->kv_row_bytes, (int64_t)b.send_idx.size() * P->in_row_bytes);
+    if (ag) sbytes = std::max(P->n_max * P->kv_row_bytes, P->n_max * P->in_row_bytes);
+    GT_TRY(P->d_send_buf.alloc((size_t)std::max<int64_t>(sbytes, 16)));
+    GT_TRY(P->d_recv_kv.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
+    GT_TRY(P->d_recv_in.alloc((size_t)std::max<int64_t>(b.recv_rows * P->in_row_bytes, 16)));
+    int64_t recv_f = 0, recv_b = 0, send_f = 0, send_b = 0;
+    for (int s = 0; s < world; ++s) {
+      if (s == P->rank) continue;
+      recv_f += f.recv_cnt[s]; recv_b += b.recv_cnt[s];
+      send_f += f.send_cnt[s]; send_b += b.send_cnt[s];
+    }
+    P->info.exch_fwd_bytes = recv_f * P->kv_row_bytes;
+    P->info.exch_bwd_bytes = recv_b * P->in_row_bytes;
+    P->info.send_fwd_bytes = send_f * P->kv_row_bytes;
+    P->info.send_bwd_bytes = send_b * P->in_row_bytes;
+  }
+
+  // ---- degree binning: rows / columns split into chunks ----
+  build_chunks(rp_local.data(), P->n_local, P->heavy_threshold, &P->heavy_rows);
+  build_chunks(P->h_col_ptr.data(), P->n_local, P->heavy_threshold, &P->heavy_cols);
+  GT_TRY(upload_chunks(P->heavy_rows));
+  GT_TRY(upload_chunks(P->heavy_cols));
+  {
+    std::vector<int32_t> ir = build_items(rp_local.data(), P->n_local, P->heavy_threshold, P->heavy_rows);
+    std::vector<int32_t> ic = build_items(P->h_col_ptr.data(), P->n_local, P->heavy_threshold, P->heavy_cols);
+    P->n_items_rows = (int64_t)ir.size();
+    P->n_items_cols = (int64_t)ic.size();
+    GT_TRY(upload(P->d_items_rows, ir.data(), ir.size()));
+    GT_TRY(upload(P->d_items_cols, ic.data(), ic.size()));
+    GT_TRY(P->d_counters.alloc(4 * sizeof(unsigned long long)));
+  }
+  const int64_t nrc = P->heavy_rows.nchunks(), ncc = P->heavy_cols.nchunks();
+  GT_TRY(P->d_part_fwd.alloc((size_t)std::max<int64_t>(nrc, 1) * (D + 2 * heads) * sizeof(float)));
+  GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * (2 * D + heads) * sizeof(float)));
+  GT_TRY(P->d_part_colb.alloc((size_t)std::max<int64_t>(ncc, 1) * (2 * D) * sizeof(float)));
+  GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * heads * 2 * sizeof(float)));
+  GT_CUDA_TRY(cudaStreamSynchronize(st));
+
+  // ---- info ----
+  gt_plan_info& I = P->info;
+  I.world = world; I.rank = P->rank; I.strategy = P->strategy; I.dtype = P->dtype; I.heads = heads; I.d = d;
+  I.scale = P->scale; I.n = n; I.nnz = nnz; I.row_lo = P->lo; I.row_hi = P->hi; I.n_local = P->n_local;
+  I.nnz_local = P->nnz_local; I.nnz_in_local = P->nnz_in_local;
+  I.halo_out_rows = single ? 0 : (P->strategy == GT_ALLGATHER ? (int64_t)(world - 1) * P->n_max : (int64_t)P->halo_out.size());
+  I.halo_in_rows = single ? 0 : (P->strategy == GT_ALLGATHER ? (int64_t)(world - 1) * P->n_max : (int64_t)P->halo_in.size());
+  I.heavy_rows = (int64_t)P->heavy_rows.ids.size();
+  I.heavy_row_chunks = nrc;
+  I.heavy_cols = (int64_t)P->heavy_cols.ids.size();
+  I.heavy_col_chunks = ncc;
+  I.launches_fwd = launches_fwd(P.get()) + (single ? 0 : 1);
+  I.launches_bwd = launches_bwd(P.get()) + (single ? 0 : 1);
+  int64_t dev = 0;
+  for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
+                          &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
+                          &P->d_recv_kv, &P->d_recv_in})
+    dev += (int64_t)b->bytes;
+  I.device_bytes = dev;
+  *out = P.release();
+  return GT_OK;
+}
+
+gt_status gt_plan(const gt_csr* csr, int64_t n, int64_t nnz, int heads, int d, int world, const gt_opts* opts,
+                  gt_plan_t* out) {
+  gt_opts def;
+  if (!opts) {
+    gt_default_opts(&def);
+    opts = &def;
+  }
+  try {
+    return plan_impl(csr, n, nnz, heads, d, world, opts, out);
+  } catch (const std::bad_alloc&) {
+    return fail(GT_ENOMEM, "gt_plan: host allocation failed");
+  } catch (...) {
+    return fail(GT_EINVAL, "gt_plan: unexpected exception");
+  }
+}
+
+gt_status gt_plan_info_get(gt_plan_t P, gt_plan_info* out) {
+  if (!P || !out) return fail(GT_EINVAL, "gt_plan_info_get: null argument");
+  *out = P->info;
+  return GT_OK;
+}
+
+gt_status gt_plan_export(gt_plan_t P, int what, int peer, void* dst, int64_t cap, int64_t* len) {
+  if (!P || !len) return fail(GT_EINVAL, "gt_plan_export: null argument");
+  const void* src = nullptr;
+  int64_t count = 0, esz = 4;
+  std::vector<int32_t> tmp32;
+  switch (what) {
+    case GT_EXPORT_BOUNDS: src = P->bounds.data(); count = (int64_t)P->bounds.size(); esz = 8; break;
+    case GT_EXPORT_HALO_OUT: src = P->halo_out.data(); count = (int64_t)P->halo_out.size(); break;
+    case GT_EXPORT_HALO_IN: src = P->halo_in.data(); count = (int64_t)P->halo_in.size(); break;
+    case GT_EXPORT_SEND_OUT:
+    case GT_EXPORT_SEND_IN: {
+      if (peer < 0 || peer >= P->world) return fail(GT_EINVAL, "gt_plan_export: bad peer");
+      if (P->world > 1) {
+        const auto& v = what == GT_EXPORT_SEND_OUT ? P->send_out[peer] : P->send_in[peer];
+        src = v.data();
+        count = (int64_t)v.size();
+      }
+      break;
+    }
+    case GT_EXPORT_CSC_PTR: src = P->h_col_ptr.data(); count = (int64_t)P->h_col_ptr.size(); esz = 8; break;
+    case GT_EXPORT_CSC_IDX: {
+      count = P->nnz_in_local;
+      tmp32.resize((size_t)count);
+      if (count) {
+        cudaError_t e = cudaMemcpy(tmp32.data(), P->d_row.p, (size_t)count * 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return fail(GT_ECUDA, cudaGetErrorString(e));
+      }
+      if (P->world > 1) {  // undo the remap: report global row ids
+        for (auto& x : tmp32) {
+          int64_t i = x;
+          if (i < P->n_local) x = (int32_t)(i + P->lo);
+          else if (P->strategy == GT_ALLGATHER) {
+            int64_t s = (i - P->n_local) / P->n_max, off = (i - P->n_local) % P->n_max;
+            x = (int32_t)(P->bounds[s] + off);
+          } else {
+            x = P->halo_in[i - P->n_local];
+          }
+        }
+      }
+      src = tmp32.data();
+      break;
+    }
+    case GT_EXPORT_HEAVY_ROWS: src = P->heavy_rows.ids.data(); count = (int64_t)P->heavy_rows.ids.size(); break;
+    case GT_EXPORT_HEAVY_COLS: src = P->heavy_cols.ids.data(); count = (int64_t)P->heavy_cols.ids.size(); break;
+    default: return fail(GT_EINVAL, "gt_plan_export: unknown table");
+  }
+  *len = count;
+  if (dst) {
+    if (cap < count) return fail(GT_EINVAL, "gt_plan_export: cap too small");
+    if (count) std::memcpy(dst, src, (size_t)(count * esz));
+  }
+  return GT_OK;
+}
+
+static gt_status check_ptrs(gt_plan_t P, std::initializer_list<const void*> ps) {
+  if (!P) return fail(GT_EINVAL, "null plan");
+  if (P->n_local == 0) return GT_OK;
+  for (const void* p : ps) {
+    if (!p) return fail(GT_EINVAL, "null tensor pointer");
+    if (((uintptr_t)p) & 15) return fail(GT_EINVAL, "tensor pointer not 16-byte aligned");
+  }
+  return GT_OK;
+}
+
+gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse, void* stream) {
+  GT_TRY(check_ptrs(P, {q, k, v, y, lse}));
+  cudaStream_t st = (cudaStream_t)stream;
+  GT_CUDA_TRY(cudaSetDevice(P->device));
+  const void* halo = nullptr;
+  cudaEvent_t ev = nullptr;
+  if (P->world > 1) {
+    const int elt = P->dtype == GT_F32 ? 4 : 2;
+    const int64_t D = (int64_t)P->heads * P->d;
+    P->mark_begin(0, st, &ev);
+    GT_TRY(pack_kv(k, v, P->d_send_out_idx.as<int32_t>(), P->n_send_out, D, elt, P->d_send_buf.p, st));
+    if (P->strategy == GT_ALLGATHER)
+      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_kv.p, P->n_max, P->kv_row_bytes, st));
+    else
+      GT_TRY(P->comm->exchange(P->d_send_buf.p, P->so_off.data(), P->so_cnt.data(), P->d_recv_kv.p,
+                               P->ro_off.data(), P->ro_cnt.data(), P->kv_row_bytes, st));
+    halo = P->d_recv_kv.p;
+    P->mark_end(0, st, ev);
+  }
+  P->mark_begin(1, st, &ev);
+  GT_TRY(launch_fwd(P, q, k, v, halo, y, lse, st));
+  P->mark_end(1, st, ev);
+  P->fwd_done = true;
+  return GT_OK;
+}
+
+gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse, const void* dy,
+                      void* dq, void* dk, void* dv, void* stream) {
+  GT_TRY(check_ptrs(P, {q, k, v, lse, dy, dq, dk, dv}));
+  if (P->world > 1 && !P->fwd_done) return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd (halo K||V not retained)");
+  cudaStream_t st = (cudaStream_t)stream;
+  GT_CUDA_TRY(cudaSetDevice(P->device));
+  const void* halo_kv = P->world > 1 ? P->d_recv_kv.p : nullptr;
+  cudaEvent_t ev = nullptr;
+  P->mark_begin(2, st, &ev);
+  GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
+  P->mark_end(2, st, ev);
+  const void* halo_in = nullptr;
+  if (P->world > 1) {
+    P->mark_begin(3, st, &ev);
+    const int elt = P->dtype == GT_F32 ? 4 : 2;
+    const int64_t D = (int64_t)P->heads * P->d;
+    GT_TRY(pack_in(q, dy, P->d_stats.as<float>(), P->d_send_in_idx.as<int32_t>(), P->n_send_in, D, P->heads, elt,
+                   P->d_send_buf.p, st));
+    if (P->strategy == GT_ALLGATHER)
+      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_in.p, P->n_max, P->in_row_bytes, st));
+    else
+      GT_TRY(P->comm->exchange(P->d_send_buf.p, P->si_off.data(), P->si_cnt.data(), P->d_recv_in.p,
+                               P->ri_off.data(), P->ri_cnt.data(), P->in_row_bytes, st));
+    halo_in = P->d_recv_in.p;
+    P->mark_end(3, st, ev);
+  }
+  P->mark_begin(4, st, &ev);
+  GT_TRY(launch_bwd_cols(P, q, k, v, dy, halo_in, dk, dv, st));
+  P->mark_end(4, st, ev);
+  return GT_OK;
+}
+
+gt_status gt_attn_fwd_bwd_host(gt_plan_t P, const void* q, const void* k, const void* v, const void* dy, void* y,
+                               float* lse, void* dq, void* dk, void* dv, void* stream) {
+  if (!P || !q || !k || !v || !dy) return fail(GT_EINVAL, "gt_attn_fwd_bwd_host: null input");
+  cudaStream_t st = (cudaStream_t)stream;
+  GT_CUDA_TRY(cudaSetDevice(P->device));
+  const int elt = P->dtype == GT_F32 ? 4 : 2;
+  const size_t tb = (size_t)std::max<int64_t>(P->n_local, 1) * P->heads * P->d * elt;
+  const size_t lb = (size_t)std::max<int64_t>(P->n_local, 1) * P->heads * sizeof(float);
+  // staging: 0 q, 1 k, 2 v, 3 dy, 4 y, 5 lse, 6 dq, 7 dk, 8 dv
+  for (int i = 0; i < 9; ++i)
+    if (!P->h2d[i].p) GT_TRY(P->h2d[i].alloc(i == 5 ? lb : tb));
+  const size_t nb = (size_t)P->n_local * P->heads * P->d * elt;
+  const size_t nl = (size_t)P->n_local * P->heads * sizeof(float);
+  const void* in[4] = {q, k, v, dy};
+  for (int i = 0; i < 4; ++i)
+    if (nb) GT_CUDA_TRY(cudaMemcpyAsync(P->h2d[i].p, in[i], nb, cudaMemcpyHostToDevice, st));
+  GT_TRY(gt_attn_fwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[4].p, P->h2d[5].as<float>(), stream));
+  GT_TRY(gt_attn_bwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[5].as<float>(), P->h2d[3].p, P->h2d[6].p,
+                     P->h2d[7].p, P->h2d[8].p, stream));
+  void* outs[5] = {y, lse, dq, dk, dv};
+  const int idx[5] = {4, 5, 6, 7, 8};
+  for (int i = 0; i < 5; ++i)
+    if (outs[i] && nb)
+      GT_CUDA_TRY(cudaMemcpyAsync(outs[i], P->h2d[idx[i]].p, idx[i] == 5 ? nl : nb, cudaMemcpyDeviceToHost, st));
+  GT_CUDA_TRY(cudaStreamSynchronize(st));
+  return GT_OK;
+}
+
+gt_status gt_plan_timings(gt_plan_t P, double* ms, int64_t* calls) {
+  if (!P || !ms) return fail(GT_EINVAL, "gt_plan_timings: null argument");
+  for (int i = 0; i < 5; ++i) {
+    ms[i] = 0;
+    if (calls) calls[i] = 0;
+  }
+  for (auto& r : P->recs) {
+    GT_CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0;
+    GT_CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.stage] += t;
+    if (calls) calls[r.stage]++;
+    P->ev_pool.push_back(r.a);
+    P->ev_pool.push_back(r.b);
+  }
+  P->recs.clear();
+  return GT_OK;
+}
+
+void gt_free(gt_plan_t P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  cudaDeviceSynchronize();
+  delete P;
+}
+
+}  // extern "C"

@@ -1,0 +1,371 @@
+// Exchange layer: pack kernels, NCCL transport (loaded at run time), in-process loopback transport.
+//
+// Forward exchange (Alg. 1 lines 2 and 5): K||V rows of remote columns, packed
+// [k | v] per row.  Backward exchange (reading Z11, transposed owner): Q||dY||(LSE2, D) rows of
+// in-neighbour rows, packed [q | dy | stats] per row, padded to 16 bytes.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gt_internal.h"
+
+// ------------------------------------------------------------------ packing --
+namespace gt {
+namespace {
+
+__global__ void pack_kv_kernel(const uint4* k, const uint4* v, const int32_t* idx, int64_t rows, int vec,
+                               uint4* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nw) {
+    const int64_t src = idx[r];
+    uint4* o = out + r * 2 * vec;
+    for (int c = lane; c < vec; c += 32) {
+      o[c] = k[src * vec + c];
+      o[vec + c] = v[src * vec + c];
+    }
+  }
+}
+
+__global__ void pack_in_kernel(const uint4* q, const uint4* dy, const float2* stats, const int32_t* idx,
+                               int64_t rows, int vec, int heads, int64_t row_vec, uint4* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nw) {
+    const int64_t src = idx[r];
+    uint4* o = out + r * row_vec;
+    for (int c = lane; c < vec; c += 32) {
+      o[c] = q[src * vec + c];
+      o[vec + c] = dy[src * vec + c];
+    }
+    float2* so = reinterpret_cast<float2*>(o + 2 * vec);
+    if (lane < heads) so[lane] = stats[src * heads + lane];
+  }
+}
+
+}  // namespace
+
+gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt, void* out,
+                  cudaStream_t st) {
+  if (rows <= 0) return GT_OK;
+  const int vec = (int)(D * elt / 16);
+  int64_t blocks = std::min<int64_t>((rows + 7) / 8, 148 * 16);
+  pack_kv_kernel<<<(int)blocks, 256, 0, st>>>((const uint4*)k, (const uint4*)v, idx, rows, vec, (uint4*)out);
+  GT_CUDA_TRY(cudaGetLastError());
+  return GT_OK;
+}
+
+gt_status pack_in(const void* q, const void* dy, const float* stats, const int32_t* idx, int64_t rows, int64_t D,
+                  int heads, int elt, void* out, cudaStream_t st) {
+  if (rows <= 0) return GT_OK;
+  const int vec = (int)(D * elt / 16);
+  const int64_t row_bytes = (2 * D * elt + 8 * heads + 15) / 16 * 16;
+  int64_t blocks = std::min<int64_t>((rows + 7) / 8, 148 * 16);
+  pack_in_kernel<<<(int)blocks, 256, 0, st>>>((const uint4*)q, (const uint4*)dy, (const float2*)stats, idx, rows,
+                                               vec, heads, row_bytes / 16, (uint4*)out);
+  GT_CUDA_TRY(cudaGetLastError());
+  return GT_OK;
+}
+
+// -------------------------------------------------------------------- NCCL --
+namespace {
+
+typedef void* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclUint8 = 1, ncclInt32 = 2, ncclFloat64 = 8 };
+enum { ncclSum = 0, ncclMax = 2 };
+
+struct NcclApi {
+  bool loaded = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("GT_NCCL_LIB");
+    void* h = nullptr;
+    if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { api.err = "libnccl.so.2 not found (set GT_NCCL_LIB)"; return; }
+#define GT_SYM(name) api.name = (decltype(api.name))dlsym(h, "nccl" #name)
+    GT_SYM(GetUniqueId); GT_SYM(CommInitRank); GT_SYM(CommDestroy); GT_SYM(AllGather); GT_SYM(AllReduce);
+    GT_SYM(Broadcast); GT_SYM(Send); GT_SYM(Recv); GT_SYM(GroupStart); GT_SYM(GroupEnd); GT_SYM(GetErrorString);
+#undef GT_SYM
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.Send || !api.Recv || !api.GroupStart ||
+        !api.GroupEnd || !api.Broadcast || !api.AllReduce) {
+      api.err = "libnccl is missing required symbols";
+      return;
+    }
+    api.loaded = true;
+  });
+  return api;
+}
+
+#define GT_NCCL_TRY(expr)                                                                            \
+  do {                                                                                               \
+    ncclResult_t _r = (expr);                                                                        \
+    if (_r != 0)                                                                                     \
+      return ::gt::fail(GT_ENCCL, std::string(#expr) + ": " +                                        \
+                                      (nccl().GetErrorString ? nccl().GetErrorString(_r) : "error")); \
+  } while (0)
+
+struct NcclComm : Comm {
+  ncclComm_t c;
+  int w, r;
+  DevBuf scratch;
+  NcclComm(ncclComm_t c_, int w_, int r_) : c(c_), w(w_), r(r_) {}
+  int world() const override { return w; }
+  int rank() const override { return r; }
+  gt_status exchange(const void* send_buf, const int64_t* send_off, const int64_t* send_cnt, void* recv_buf,
+                     const int64_t* recv_off, const int64_t* recv_cnt, int64_t row_bytes,
+                     cudaStream_t stream) override {
+    NcclApi& a = nccl();
+    GT_NCCL_TRY(a.GroupStart());
+    for (int s = 0; s < w; ++s) {
+      if (s == r) continue;
+      if (send_cnt[s] > 0)
+        GT_NCCL_TRY(a.Send((const char*)send_buf + send_off[s] * row_bytes, (size_t)(send_cnt[s] * row_bytes),
+                           ncclUint8, s, c, stream));
+      if (recv_cnt[s] > 0)
+        GT_NCCL_TRY(a.Recv((char*)recv_buf + recv_off[s] * row_bytes, (size_t)(recv_cnt[s] * row_bytes), ncclUint8,
+                           s, c, stream));
+    }
+    GT_NCCL_TRY(a.GroupEnd());
+    return GT_OK;
+  }
+  gt_status all_gather(const void* send_buf, void* recv_buf, int64_t rows, int64_t row_bytes,
+                       cudaStream_t stream) override {
+    if (rows == 0) return GT_OK;
+    GT_NCCL_TRY(nccl().AllGather(send_buf, recv_buf, (size_t)(rows * row_bytes), ncclUint8, c, stream));
+    return GT_OK;
+  }
+  gt_status ensure_scratch() {
+    if (!scratch.p) GT_TRY(scratch.alloc(4096));
+    return GT_OK;
+  }
+  gt_status broadcast_host(void* data, int64_t bytes, cudaStream_t stream) override {
+    GT_TRY(ensure_scratch());
+    if (bytes > 4096) return fail(GT_EINVAL, "broadcast_host: too large");
+    GT_CUDA_TRY(cudaMemcpyAsync(scratch.p, data, bytes, cudaMemcpyHostToDevice, stream));
+    GT_NCCL_TRY(nccl().Broadcast(scratch.p, scratch.p, (size_t)bytes, ncclUint8, 0, c, stream));
+    GT_CUDA_TRY(cudaMemcpyAsync(data, scratch.p, bytes, cudaMemcpyDeviceToHost, stream));
+    GT_CUDA_TRY(cudaStreamSynchronize(stream));
+    return GT_OK;
+  }
+  gt_status max_host(double* v, cudaStream_t stream) override {
+    GT_TRY(ensure_scratch());
+    GT_CUDA_TRY(cudaMemcpyAsync(scratch.p, v, sizeof(double), cudaMemcpyHostToDevice, stream));
+    GT_NCCL_TRY(nccl().AllReduce(scratch.p, scratch.p, 1, ncclFloat64, ncclMax, c, stream));
+    GT_CUDA_TRY(cudaMemcpyAsync(v, scratch.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    GT_CUDA_TRY(cudaStreamSynchronize(stream));
+    return GT_OK;
+  }
+  gt_status barrier(cudaStream_t stream) override {
+    double x = 0;
+    return max_host(&x, stream);
+  }
+};
+
+}  // namespace
+
+Comm* make_nccl_comm(void* nccl_comm, int world, int rank, gt_status* st) {
+  if (!nccl().loaded) {
+    *st = fail(GT_ENCCL, nccl().err);
+    return nullptr;
+  }
+  *st = GT_OK;
+  return new NcclComm((ncclComm_t)nccl_comm, world, rank);
+}
+
+}  // namespace gt
+
+// ---------------------------------------------------------------- loopback --
+struct gt_loopback_s {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  struct Slot {
+    const void* send = nullptr;
+    const int64_t* off = nullptr;
+    const int64_t* cnt = nullptr;
+    int64_t row_bytes = 0;
+    cudaEvent_t ready = nullptr, done = nullptr;
+    std::vector<char> host;
+    double val = 0;
+  };
+  std::vector<Slot> slots;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+namespace gt {
+namespace {
+
+struct LoopbackComm : Comm {
+  gt_loopback_s* g;
+  int r;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  std::vector<int64_t> ag_off, ag_cnt, ag_roff;
+  LoopbackComm(gt_loopback_s* g_, int r_) : g(g_), r(r_) {
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  }
+  ~LoopbackComm() override {
+    if (ready) cudaEventDestroy(ready);
+    if (done) cudaEventDestroy(done);
+  }
+  int world() const override { return g->world; }
+  int rank() const override { return r; }
+  gt_status exchange(const void* send_buf, const int64_t* send_off, const int64_t* send_cnt, void* recv_buf,
+                     const int64_t* recv_off, const int64_t* recv_cnt, int64_t row_bytes,
+                     cudaStream_t stream) override {
+    const int w = g->world;
+    GT_CUDA_TRY(cudaEventRecord(ready, stream));
+    auto& me = g->slots[r];
+    me.send = send_buf; me.off = send_off; me.cnt = send_cnt; me.row_bytes = row_bytes; me.ready = ready;
+    g->barrier();
+    gt_status st = GT_OK;
+    for (int s = 0; s < w && st == GT_OK; ++s) {
+      if (s == r) continue;
+      const auto& peer = g->slots[s];
+      if (peer.row_bytes != row_bytes || peer.cnt[r] != recv_cnt[s]) {
+        st = fail(GT_ENCCL, "loopback exchange: protocol mismatch between ranks " + std::to_string(r) + " and " +
+                                std::to_string(s));
+        break;
+      }
+      if (recv_cnt[s] == 0) continue;
+      if (cudaStreamWaitEvent(stream, peer.ready, 0) != cudaSuccess ||
+          cudaMemcpyAsync((char*)recv_buf + recv_off[s] * row_bytes, (const char*)peer.send + peer.off[r] * row_bytes,
+                          (size_t)(recv_cnt[s] * row_bytes), cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+        st = fail(GT_ECUDA, "loopback exchange: copy failed");
+    }
+    cudaEventRecord(done, stream);
+    me.done = done;
+    g->barrier();
+    for (int s = 0; s < w; ++s)
+      if (s != r) cudaStreamWaitEvent(stream, g->slots[s].done, 0);
+    g->barrier();
+    return st;
+  }
+  gt_status all_gather(const void* send_buf, void* recv_buf, int64_t rows, int64_t row_bytes,
+                       cudaStream_t stream) override {
+    const int w = g->world;
+    ag_off.assign(w, 0);
+    ag_cnt.assign(w, rows);
+    ag_roff.resize(w);
+    for (int s = 0; s < w; ++s) ag_roff[s] = s * rows;
+    if (rows > 0)
+      GT_CUDA_TRY(cudaMemcpyAsync((char*)recv_buf + r * rows * row_bytes, send_buf, (size_t)(rows * row_bytes),
+                                  cudaMemcpyDeviceToDevice, stream));
+    return exchange(send_buf, ag_off.data(), ag_cnt.data(), recv_buf, ag_roff.data(), ag_cnt.data(), row_bytes,
+                    stream);
+  }
+  gt_status broadcast_host(void* data, int64_t bytes, cudaStream_t) override {
+    if (r == 0) g->slots[0].host.assign((const char*)data, (const char*)data + bytes);
+    g->barrier();
+    std::memcpy(data, g->slots[0].host.data(), (size_t)bytes);
+    g->barrier();
+    return GT_OK;
+  }
+  gt_status max_host(double* v, cudaStream_t) override {
+    g->slots[r].val = *v;
+    g->barrier();
+    double m = *v;
+    for (int s = 0; s < g->world; ++s) m = std::max(m, g->slots[s].val);
+    g->barrier();
+    *v = m;
+    return GT_OK;
+  }
+  gt_status barrier(cudaStream_t) override {
+    g->barrier();
+    return GT_OK;
+  }
+};
+
+}  // namespace
+
+Comm* make_loopback_comm(gt_loopback_t g, int world, int rank, gt_status* st) {
+  if (!g || g->world != world) {
+    *st = fail(GT_EINVAL, "loopback group size does not match world");
+    return nullptr;
+  }
+  *st = GT_OK;
+  return new LoopbackComm(g, rank);
+}
+
+}  // namespace gt
+
+using namespace gt;
+
+extern "C" {
+
+gt_status gt_loopback_create(int world, gt_loopback_t* out) {
+  if (world < 1 || !out) return fail(GT_EINVAL, "gt_loopback_create: bad arguments");
+  auto* g = new gt_loopback_s();
+  g->world = world;
+  g->slots.resize(world);
+  *out = g;
+  return GT_OK;
+}
+
+void gt_loopback_destroy(gt_loopback_t g) { delete g; }
+
+gt_status gt_nccl_unique_id(void* uid128) {
+  if (!uid128) return fail(GT_EINVAL, "null uid");
+  if (!nccl().loaded) return fail(GT_ENCCL, nccl().err);
+  ncclUniqueId id;
+  GT_NCCL_TRY(nccl().GetUniqueId(&id));
+  std::memcpy(uid128, &id, sizeof(id));
+  return GT_OK;
+}
+
+gt_status gt_nccl_comm_create(const void* uid128, int world, int rank, void** comm) {
+  if (!uid128 || !comm || world < 1 || rank < 0 || rank >= world) return fail(GT_EINVAL, "bad arguments");
+  if (!nccl().loaded) return fail(GT_ENCCL, nccl().err);
+  ncclUniqueId id;
+  std::memcpy(&id, uid128, sizeof(id));
+  ncclComm_t c = nullptr;
+  GT_NCCL_TRY(nccl().CommInitRank(&c, world, id, rank));
+  *comm = c;
+  return GT_OK;
+}
+
+void gt_nccl_comm_destroy(void* comm) {
+  if (comm && nccl().loaded && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)comm);
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// Internal declarations of libgt.so (not part of the ABI; see include/gt.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gt.h"
+
+namespace gt {
+
+// ------------------------------------------------------------------ errors --
+void set_error(const std::string& msg);
+gt_status fail(gt_status s, const std::string& msg);
+
+#define GT_CUDA_TRY(expr)                                                                  \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return ::gt::fail(GT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+#define GT_TRY(expr)                 \
+  do {                               \
+    gt_status _s = (expr);           \
+    if (_s != GT_OK) return _s;      \
+  } while (0)
+
+// ------------------------------------------------------------- device memory --
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  gt_status alloc(size_t n);
+  void release();
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+  ~DevBuf() { release(); }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// ------------------------------------------------------------------- comm --
+// Transport for the two exchanges of a step (forward K||V rows, backward Q||dY||stats rows).
+// A "pattern" is an all-to-all-v of fixed-size rows: send_cnt[s] rows to peer s from
+// send_buf + send_off[s] rows, recv_cnt[s] rows from peer s into recv_buf + recv_off[s] rows.
+struct Comm {
+  virtual ~Comm() = default;
+  virtual int world() const = 0;
+  virtual int rank() const = 0;
+  // all-to-all-v of rows of `row_bytes` bytes, enqueued on `stream`.
+  virtual gt_status exchange(const void* send_buf, const int64_t* send_off, const int64_t* send_cnt,
+                             void* recv_buf, const int64_t* recv_off, const int64_t* recv_cnt,
+                             int64_t row_bytes, cudaStream_t stream) = 0;
+  // all-gather of `rows` rows per rank (padded blocks): recv_buf is [world, rows, row_bytes].
+  virtual gt_status all_gather(const void* send_buf, void* recv_buf, int64_t rows, int64_t row_bytes,
+                               cudaStream_t stream) = 0;
+  // broadcast of a small host value from rank 0 (host-synchronous).
+  virtual gt_status broadcast_host(void* data, int64_t bytes, cudaStream_t stream) = 0;
+  // max over ranks of a host double (host-synchronous).
+  virtual gt_status max_host(double* v, cudaStream_t stream) = 0;
+  virtual gt_status barrier(cudaStream_t stream) = 0;
+};
+
+Comm* make_nccl_comm(void* nccl_comm, int world, int rank, gt_status* st);
+Comm* make_loopback_comm(gt_loopback_t g, int world, int rank, gt_status* st);
+
+// ------------------------------------------------------------------- plan --
+struct ChunkTable {        // rows (or columns) split into chunks of <= chunk edges
+  std::vector<int32_t> ids;        // local ids of heavy rows/cols, ascending
+  std::vector<int32_t> first;      // first chunk of each heavy id (size ids.size() + 1)
+  std::vector<int64_t> chunk_lo;   // [nchunks] entry range start (offset in the CSR/CSC slice)
+  std::vector<int64_t> chunk_hi;
+  std::vector<int32_t> chunk_owner;// [nchunks] local row/col id
+  DevBuf d_ids, d_first, d_lo, d_hi, d_owner;
+  int64_t nchunks() const { return (int64_t)chunk_lo.size(); }
+};
+
+}  // namespace gt
+
+struct gt_plan_s {
+  // identity
+  int world = 1, rank = 0, heads = 0, d = 0, dtype = GT_BF16, strategy = GT_SINGLE, device = 0;
+  float scale = 0.f;
+  int64_t n = 0, nnz = 0;
+  int heavy_threshold = 1024;
+  std::vector<int64_t> bounds;     // [world + 1]
+  int64_t lo = 0, hi = 0, n_local = 0, nnz_local = 0, nnz_in_local = 0;
+
+  // row pass (forward, backward dQ): local CSR over owned rows, columns remapped
+  gt::DevBuf d_row_ptr;            // int64[n_local + 1], rebased to 0
+  gt::DevBuf d_col;                // int32[nnz_local]: < n_local local row; >= n_local halo slot
+  // column pass (dK, dV): CSC of owned columns, rows remapped the same way (halo-in slots)
+  gt::DevBuf d_col_ptr;            // int64[n_local + 1], rebased to 0
+  gt::DevBuf d_row;                // int32[nnz_in_local]
+  std::vector<int64_t> h_col_ptr;  // host copy of d_col_ptr (exports, chunking)
+
+  gt::ChunkTable heavy_rows, heavy_cols;
+  // work items in row (column) order: id >= 0 a whole row, id < 0 chunk (-1 - id) of a heavy row
+  gt::DevBuf d_items_rows, d_items_cols, d_counters;
+  int64_t n_items_rows = 0, n_items_cols = 0;
+
+  // backward statistics: [n_local, heads, 2] fp32 = (LSE * log2(e), D)
+  gt::DevBuf d_stats;
+  // heavy-chunk workspaces (fp32)
+  gt::DevBuf d_part_fwd;           // [row chunks, D + 2 heads]
+  gt::DevBuf d_part_rowb;          // [row chunks, 2 D + heads]
+  gt::DevBuf d_part_colb;          // [col chunks, 2 D]
+
+  // multi-rank exchange
+  gt::Comm* comm = nullptr;
+  bool own_comm = true;
+  std::vector<int32_t> halo_out, halo_in;                 // global ids, ascending
+  std::vector<std::vector<int32_t>> send_out, send_in;    // [peer] global ids
+  std::vector<int64_t> so_off, so_cnt, ro_off, ro_cnt;    // forward pattern (rows)
+  std::vector<int64_t> si_off, si_cnt, ri_off, ri_cnt;    // backward pattern (rows)
+  int64_t n_max = 0;               // all-gather block rows
+  int64_t n_send_out = 0, n_send_in = 0;                  // rows packed per exchange
+  int64_t halo_out_rows = 0, halo_in_rows = 0;            // rows of the receive tables
+  gt::DevBuf d_send_out_idx, d_send_in_idx;               // int32 local ids to pack
+  gt::DevBuf d_send_buf, d_recv_kv, d_recv_in;            // packed rows
+  int64_t kv_row_bytes = 0, in_row_bytes = 0;
+  bool fwd_done = false;
+
+  // end-to-end host staging
+  gt::DevBuf h2d[9];
+
+  gt_plan_info info{};
+  cudaStream_t side = nullptr;
+
+  // stage profiling (opts.profile)
+  bool profile = false;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t take_event();
+  void mark_begin(int stage, cudaStream_t st, cudaEvent_t* a);
+  void mark_end(int stage, cudaStream_t st, cudaEvent_t a);
+  ~gt_plan_s();
+};
+
+namespace gt {
+// attention kernels (attn.cu)
+gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv, void* y,
+                     float* lse, cudaStream_t st);
+gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
+                          const float* lse, const void* dy, void* dq, cudaStream_t st);
+gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
+                          const void* halo_in, void* dk, void* dv, cudaStream_t st);
+bool shape_supported(int heads, int d, int dtype);
+int launches_fwd(const gt_plan_s* P);
+int launches_bwd(const gt_plan_s* P);
+
+// pack kernels (comm.cu)
+gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,
+                  void* out, cudaStream_t st);
+gt_status pack_in(const void* q, const void* dy, const float* stats, const int32_t* idx, int64_t rows,
+                  int64_t D, int heads, int elt, void* out, cudaStream_t st);
+
+// graph (graph.cu)
+gt_status build_csc_device(const int64_t* d_row_ptr, const int32_t* d_col, int64_t n, int64_t nnz,
+                           int64_t* d_col_ptr, int32_t* d_row, cudaStream_t st);
+
+// host helpers (host.cpp)
+gt_status validate_csr(const int64_t* row_ptr, const int32_t* col_idx, int64_t n, int64_t nnz);
+void partition_rows(int64_t n, const int64_t* row_ptr, int p, int mode, int64_t* bounds);
+std::vector<int32_t> halo_set(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t lo, int64_t hi,
+                              bool inward);
+// Rows this rank (owning [lo, hi)) sends to the rank owning [blo, bhi):
+//   inward = 0 (forward): owned columns referenced by rows in [blo, bhi)   = H_peer  n [lo, hi)
+//   inward = 1 (backward): owned rows with an entry in a column of [blo, bhi) = H_peer^in n [lo, hi)
+std::vector<int32_t> send_set(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t lo, int64_t hi,
+                              int64_t blo, int64_t bhi, bool inward);
+void build_chunks(const int64_t* ptr, int64_t count, int64_t threshold, ChunkTable* t);
+std::vector<int32_t> build_items(const int64_t* ptr, int64_t count, int64_t threshold, const ChunkTable& t);
+}  // namespace gt

@@ -23,6 +23,9 @@ def gpu_available() -> bool:
 
 def pytest_collection_modifyitems(config, items):
     if gpu_available():
+        # (re)build every native component in-tree before GPU tests; no-op when up to date
+        import __graft_entry__
+        __graft_entry__.build()
         return
     skip = pytest.mark.skip(reason="no CUDA device")
     for it in items:

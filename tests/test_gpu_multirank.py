@@ -1,0 +1,116 @@
+"""Multi-rank path on one GPU: `world` host threads, each a rank with its own plan, exchanging rows
+through the in-process loopback transport (device-to-device copies on each rank's stream).
+
+Checks: outputs of all ranks, concatenated in row order, match the fp64 oracle within the
+single-GPU tolerances; bounds, halo sets and send lists match the oracle bit-exactly; both
+strategies (all-gather, halo) and the cost-model choice (auto).
+"""
+import math
+import threading
+
+import numpy as np
+import pytest
+
+import gtgen
+import oracle
+from tests._util import TOL, check_lse, inputs, normwise, to_f64, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0):
+    import torch
+    import paper_2604_16715_b200 as gt
+    n = len(rp) - 1
+    q, k, v, dy = inputs(n, h, d, dtype, seed)
+    scale = 1.0 / math.sqrt(h * d)
+    grp = gt.LoopbackGroup(world)
+    res = [None] * world
+    errors = []
+    full = [to_torch(x) for x in (q, k, v, dy)]
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, world=world, rank=r, comm=grp,
+                           strategy=strategy, heavy_threshold=heavy, partition=partition)
+            lo, hi = plan.row_lo, plan.row_hi
+            with torch.cuda.stream(s):
+                tq, tk, tv, tdy = (t[lo:hi].contiguous() for t in full)
+            s.synchronize()
+            y, lse = plan.fwd(tq, tk, tv, stream=s)
+            dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy, stream=s)
+            s.synchronize()
+            ex = {w: plan.export(w) for w in ("bounds", "halo_out", "halo_in")}
+            ex["send_out"] = [plan.export("send_out", p) for p in range(world)]
+            ex["send_in"] = [plan.export("send_in", p) for p in range(world)]
+            ex["csc_ptr"], ex["csc_idx"] = plan.export("csc_ptr"), plan.export("csc_idx")
+            res[r] = (lo, hi, [to_f64(t) for t in (y, lse, dq, dk, dv)], ex, plan.info())
+            plan.close()
+        except Exception as e:  # surfaced below
+            errors.append((r, e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    grp.close()
+    assert not errors, errors
+    return (q, k, v, dy, scale), res
+
+
+def check(rp, ci, dtype, ins, res, world, partition=0):
+    q, k, v, dy, scale = ins
+    Y, LSE = oracle.forward(rp, ci, q, k, v, scale)
+    DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, scale)
+    outs = [np.concatenate([r[2][i] for r in res]) for i in range(5)]
+    for name, got, ref in (("y", outs[0], Y), ("dq", outs[2], DQ), ("dk", outs[3], DK), ("dv", outs[4], DV)):
+        e = normwise(got, ref)
+        assert e <= TOL[dtype], f"{name}: {e}"
+    check_lse(outs[1], LSE, dtype)
+    bounds = oracle.partition(rp, world, partition)
+    cp, ri = oracle.transpose(rp, ci)
+    for r, (lo, hi, _, ex, info) in enumerate(res):
+        np.testing.assert_array_equal(ex["bounds"], bounds)
+        assert (lo, hi) == (bounds[r], bounds[r + 1])
+        np.testing.assert_array_equal(ex["halo_out"], oracle.halo(rp, ci, lo, hi))
+        np.testing.assert_array_equal(ex["halo_in"], oracle.halo(rp, ci, lo, hi, inward=True))
+        for p in range(world):
+            if p == r:
+                continue
+            hp = oracle.halo(rp, ci, bounds[p], bounds[p + 1])
+            hpi = oracle.halo(rp, ci, bounds[p], bounds[p + 1], inward=True)
+            np.testing.assert_array_equal(ex["send_out"][p], oracle.send_list(hp, bounds, r))
+            np.testing.assert_array_equal(ex["send_in"][p], oracle.send_list(hpi, bounds, r))
+        # owned-column slice of A^T, global row ids
+        np.testing.assert_array_equal(ex["csc_ptr"], cp[lo:hi + 1] - cp[lo])
+        np.testing.assert_array_equal(ex["csc_idx"], ri[cp[lo]:cp[hi]])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("strategy", ["halo", "allgather"])
+def test_loopback_directed_power_law(world, strategy):
+    rp, ci = gtgen.random_graph(2500, 30000, seed=70 + world, directed=True, power=2.1)
+    ins, res = run_loopback(rp, ci, 4, 64, "bf16", world, strategy, seed=700 + world, heavy=64)
+    check(rp, ci, "bf16", ins, res, world)
+    for r in res:
+        assert r[4]["strategy_name"] == strategy
+
+
+def test_loopback_communities_f32_auto():
+    rp, ci = gtgen.random_graph(4096, 50000, seed=81, directed=False, power=2.2, comm_size=512, f_in=0.9)
+    ins, res = run_loopback(rp, ci, 8, 16, "f32", 4, "auto", seed=801)
+    check(rp, ci, "f32", ins, res, 4)
+    chosen = {r[4]["strategy_name"] for r in res}
+    assert len(chosen) == 1 and chosen <= {"halo", "allgather"}  # every rank applies rank 0's decision
+
+
+def test_loopback_more_ranks_than_rows_and_node_partition():
+    rp, ci = gtgen.csr_from_pairs(3, [(0, 1), (1, 2), (2, 0), (2, 1)])
+    ins, res = run_loopback(rp, ci, 2, 64, "f32", 5, "halo", seed=901)
+    check(rp, ci, "f32", ins, res, 5)
+    rp, ci = gtgen.random_graph(700, 6000, seed=91, power=2.3)
+    ins, res = run_loopback(rp, ci, 4, 32, "bf16", 3, "allgather", seed=902, partition=1)
+    check(rp, ci, "bf16", ins, res, 3, partition=1)

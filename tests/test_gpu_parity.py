@@ -1,0 +1,171 @@
+"""GPU parity: libgt (C ABI, CUDA sm_100a) vs the fp64 CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star; reading Z8): normwise max relative error <= 1e-4 (fp32) and
+<= 2e-2 (bf16) for Y, dQ, dK, dV; LSE absolute <= 1e-4 / 1e-2 with -inf exactly on empty rows;
+integer tables (CSC) bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gtgen
+import oracle
+from tests._util import TOL, check_lse, inputs, normwise, to_f64, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gt():
+    import paper_2604_16715_b200 as g
+    return g
+
+
+def run_case(gt, row_ptr, col_idx, h, d, dtype, seed, scale=None, qk_scale=1.0, heavy=0, q_zero=False):
+    import torch
+    n = len(row_ptr) - 1
+    q, k, v, dy = inputs(n, h, d, dtype, seed, qk_scale)
+    if q_zero:
+        q = np.zeros_like(q)
+    scale = scale if scale is not None else 1.0 / math.sqrt(h * d)
+    plan = gt.Plan(row_ptr, col_idx, h, d, dtype=dtype, scale=scale, heavy_threshold=heavy)
+    tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
+    y, lse = plan.fwd(tq, tk, tv)
+    dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy)
+    torch.cuda.synchronize()
+    Y, LSE = oracle.forward(row_ptr, col_idx, q, k, v, scale)
+    DQ, DK, DV, _ = oracle.backward(row_ptr, col_idx, q, k, v, dy, scale)
+    errs = {"y": normwise(to_f64(y), Y), "dq": normwise(to_f64(dq), DQ), "dk": normwise(to_f64(dk), DK),
+            "dv": normwise(to_f64(dv), DV)}
+    check_lse(to_f64(lse), LSE, dtype)
+    for name, e in errs.items():
+        assert e <= TOL[dtype], f"{name}: normwise error {e:.3e} > {TOL[dtype]}"
+    return plan, errs, (tq, tk, tv, tdy), (y, lse, dq, dk, dv)
+
+
+def test_c1_cora_f32(gt):
+    c = gtgen.CONFIGS["C1"]
+    rp, ci = gtgen.make_graph(c.graph)
+    run_case(gt, rp, ci, c.heads, c.d, c.dtype, seed=101)
+
+
+def test_c2_arxiv_bf16(gt):
+    c = gtgen.CONFIGS["C2"]
+    rp, ci = gtgen.make_graph(c.graph)
+    run_case(gt, rp, ci, c.heads, c.d, c.dtype, seed=102)
+
+
+SHAPES = [  # h, d, dtype
+    (4, 64, "bf16"), (4, 64, "f32"), (8, 16, "f32"), (8, 32, "bf16"), (1, 128, "bf16"), (2, 64, "f32"),
+    (2, 256, "bf16"), (8, 64, "f32"), (1, 256, "f32"), (4, 32, "bf16"),
+]
+
+
+@pytest.mark.parametrize("h,d,dtype", SHAPES)
+def test_shapes_power_law_with_chunking(gt, h, d, dtype):
+    rp, ci = gtgen.random_graph(3000, 45000, seed=7 + h + d, directed=True, power=2.05)
+    run_case(gt, rp, ci, h, d, dtype, seed=200 + h * d, heavy=48)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_peaked_softmax_logits_x8(gt, dtype):
+    rp, ci = gtgen.random_graph(2000, 30000, seed=31, power=2.2)
+    run_case(gt, rp, ci, 4, 64, dtype, seed=301, scale=8.0 / math.sqrt(64), heavy=64)
+
+
+def test_all_equal_logits(gt):
+    rp, ci = gtgen.random_graph(1500, 20000, seed=32, power=2.2)
+    run_case(gt, rp, ci, 4, 64, "f32", seed=302, q_zero=True, heavy=40)
+
+
+def test_empty_graph_and_isolated_rows(gt):
+    n = 37
+    rp = np.zeros(n + 1, np.int64)
+    ci = np.zeros(0, np.int32)
+    plan, errs, ins, outs = run_case(gt, rp, ci, 4, 32, "bf16", seed=303)
+    y, lse, dq, dk, dv = outs
+    assert float(y.abs().max()) == 0.0 and float(dq.abs().max()) == 0.0
+    assert float(dk.abs().max()) == 0.0 and float(dv.abs().max()) == 0.0
+
+
+def test_single_edge_and_star(gt):
+    rp, ci = gtgen.csr_from_pairs(5, [(3, 1)])
+    run_case(gt, rp, ci, 2, 64, "f32", seed=304)
+    n = 700  # hub row 0 -> all, all -> hub column 0: exercises chunked rows and chunked columns
+    pairs = [(0, j) for j in range(1, n)] + [(j, 0) for j in range(1, n)]
+    rp, ci = gtgen.csr_from_pairs(n, pairs)
+    plan, *_ = run_case(gt, rp, ci, 4, 64, "bf16", seed=305, heavy=100)
+    inf = plan.info()
+    assert inf["heavy_rows"] == 1 and inf["heavy_cols"] == 1 and inf["heavy_row_chunks"] == 7
+
+
+def test_one_row_single_node(gt):
+    rp, ci = gtgen.csr_from_pairs(1, [(0, 0)])
+    run_case(gt, rp, ci, 1, 128, "f32", seed=306)
+
+
+def test_csc_bitexact_and_deterministic(gt):
+    import torch
+    rp, ci = gtgen.random_graph(5000, 80000, seed=41, power=2.1)
+    plan, errs, ins, outs = run_case(gt, rp, ci, 4, 64, "bf16", seed=401, heavy=128)
+    cp, ri = oracle.transpose(rp, ci)
+    np.testing.assert_array_equal(plan.export("csc_ptr"), cp)
+    np.testing.assert_array_equal(plan.export("csc_idx"), ri)
+    # bitwise run-to-run determinism (no atomics in the numerics)
+    tq, tk, tv, tdy = ins
+    y2, lse2 = plan.fwd(tq, tk, tv)
+    dq2, dk2, dv2 = plan.bwd(tq, tk, tv, lse2, tdy)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, (y2, lse2, dq2, dk2, dv2)):
+        assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
+                           b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
+
+
+def test_autograd_wrapper(gt):
+    import torch
+    rp, ci = gtgen.random_graph(800, 9000, seed=51, power=2.3)
+    h, d = 4, 32
+    q, k, v, dy = inputs(800, h, d, "f32", 501)
+    plan = gt.Plan(rp, ci, h, d, dtype="f32")
+    tq, tk, tv = (to_torch(x).requires_grad_(True) for x in (q, k, v))
+    y = gt.sparse_graph_attention(plan, tq, tk, tv)
+    y.backward(to_torch(dy))
+    DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, plan.scale)
+    assert normwise(to_f64(tq.grad), DQ) <= 1e-4
+    assert normwise(to_f64(tk.grad), DK) <= 1e-4
+    assert normwise(to_f64(tv.grad), DV) <= 1e-4
+
+
+def test_host_buffer_entry_point(gt):
+    import torch
+    rp, ci = gtgen.random_graph(1200, 15000, seed=61, power=2.2)
+    h, d = 4, 64
+    q, k, v, dy = inputs(1200, h, d, "bf16", 601)
+    plan = gt.Plan(rp, ci, h, d, dtype="bf16")
+    pin = lambda x: to_torch(x, "cpu").pin_memory()  # noqa: E731
+    tq, tk, tv, tdy = (pin(x) for x in (q, k, v, dy))
+    y, dq, dk, dv = (torch.empty_like(tq).pin_memory() for _ in range(4))
+    lse = torch.empty((1200, h), dtype=torch.float32).pin_memory()
+    plan.fwd_bwd_host(tq, tk, tv, tdy, y, lse, dq, dk, dv)
+    Y, LSE = oracle.forward(rp, ci, q, k, v, plan.scale)
+    DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, plan.scale)
+    assert normwise(to_f64(y), Y) <= 2e-2 and normwise(to_f64(dq), DQ) <= 2e-2
+    assert normwise(to_f64(dk), DK) <= 2e-2 and normwise(to_f64(dv), DV) <= 2e-2
+    check_lse(lse.numpy(), LSE, "bf16")
+
+
+def test_errors_are_reported(gt):
+    rp, ci = gtgen.csr_from_pairs(4, [(0, 1), (1, 2)])
+    bad = ci.copy()
+    bad[0] = 7
+    with pytest.raises(gt.GTError) as e:
+        gt.Plan(rp, bad, 4, 64)
+    assert e.value.status == 2  # GT_EGRAPH
+    with pytest.raises(gt.GTError) as e:
+        gt.Plan(rp, ci, 3, 64)
+    assert e.value.status == 3  # GT_ECONFIG
+    unsorted = gtgen.csr_from_pairs(3, [(0, 1), (0, 2)])
+    uc = unsorted[1][::-1].copy()
+    with pytest.raises(gt.GTError):
+        gt.Plan(unsorted[0], uc, 4, 64)
