@@ -27,12 +27,12 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src: str, verbose: bool, defines=(), objdir=OBJ) -> str:
+    obj = os.path.join(objdir, os.path.basename(src) + ".o")
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(HERE, "..", "include", "gt.h"))
     if _stale(obj, [src] + headers):
-        cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -43,20 +43,21 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, objdir: str = OBJ) -> str:
+    """Compiles csrc/ into `lib`; `defines` (e.g. ["GT_FFMA2=0"]) build tuning variants."""
+    os.makedirs(objdir, exist_ok=True)
     srcs = sources()
     if force:
-        for f in os.listdir(OBJ):
-            os.remove(os.path.join(OBJ, f))
+        for f in os.listdir(objdir):
+            os.remove(os.path.join(objdir, f))
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lgomp", "-ldl", "-lpthread"]
+        objs = list(ex.map(lambda s: _compile(s, verbose, defines, objdir), srcs))
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lgomp", "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

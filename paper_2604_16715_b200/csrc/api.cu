@@ -222,6 +222,11 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   P->scale = opts->scale > 0.f ? opts->scale : (float)(1.0 / std::sqrt((double)heads * d));
   P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 1024;
   P->profile = opts->profile != 0;
+  {
+    const char* kv = getenv("GT_KERNEL");
+    P->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
+  }
+  P->stats_stride = (int)((8 * heads + 15) / 16 * 16 / 4);
   const int64_t D = (int64_t)heads * d;
   const int elt = opts->dtype == GT_F32 ? 4 : 2;
   P->kv_row_bytes = 2 * D * elt;
@@ -414,13 +419,17 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     P->n_items_cols = (int64_t)ic.size();
     GT_TRY(upload(P->d_items_rows, ir.data(), ir.size()));
     GT_TRY(upload(P->d_items_cols, ic.data(), ic.size()));
+    std::vector<int64_t> pr = build_item_ptr(rp_local.data(), P->n_local, ir, P->heavy_rows);
+    std::vector<int64_t> pc = build_item_ptr(P->h_col_ptr.data(), P->n_local, ic, P->heavy_cols);
+    GT_TRY(upload(P->d_iptr_rows, pr.data(), pr.size()));
+    GT_TRY(upload(P->d_iptr_cols, pc.data(), pc.size()));
     GT_TRY(P->d_counters.alloc(4 * sizeof(unsigned long long)));
   }
   const int64_t nrc = P->heavy_rows.nchunks(), ncc = P->heavy_cols.nchunks();
   GT_TRY(P->d_part_fwd.alloc((size_t)std::max<int64_t>(nrc, 1) * (D + 2 * heads) * sizeof(float)));
   GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * (2 * D + heads) * sizeof(float)));
   GT_TRY(P->d_part_colb.alloc((size_t)std::max<int64_t>(ncc, 1) * (2 * D) * sizeof(float)));
-  GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * heads * 2 * sizeof(float)));
+  GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->stats_stride * sizeof(float)));
   GT_CUDA_TRY(cudaStreamSynchronize(st));
 
   // ---- info ----

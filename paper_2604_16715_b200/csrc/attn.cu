@@ -35,6 +35,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 256;
+#ifndef GT_BWD_MINB
+#define GT_BWD_MINB 1
+#endif
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -49,6 +52,9 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                : "l"(p));
   return r;
 }
+
+template <int H>
+constexpr int kSBF = (8 * H + 15) / 16 * 4;  // floats per row of the (LSE2, D) stats array
 
 template <typename T, int H, int D>
 struct Cfg {
@@ -132,6 +138,60 @@ __device__ __forceinline__ void store_f32(void* row_base, int lane, const float 
   st_words<W>(static_cast<char*>(row_base) + (size_t)lane * W * 4, w);
 }
 
+// Packed fp32 math (FFMA2 / FMUL2 on sm_100a): two lanes of fp32 per instruction.
+#ifndef GT_FFMA2
+#define GT_FFMA2 1
+#endif
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+#if GT_FFMA2
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+#else
+  return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+#endif
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+#if GT_FFMA2
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+#else
+  return make_float2(a.x * b.x, a.y * b.y);
+#endif
+}
+
+// acc[i] += p * x[i]  (pairwise)
+template <int EPL>
+__device__ __forceinline__ void axpy(float p, const float (&x)[EPL], float (&acc)[EPL]) {
+  const float2 pp = make_float2(p, p);
+#pragma unroll
+  for (int i = 0; i < EPL; i += 2) {
+    float2 r = f2fma(pp, make_float2(x[i], x[i + 1]), make_float2(acc[i], acc[i + 1]));
+    acc[i] = r.x;
+    acc[i + 1] = r.y;
+  }
+}
+
+template <int EPL>
+__device__ __forceinline__ void scale_by(float c, float (&acc)[EPL]) {
+  const float2 cc = make_float2(c, c);
+#pragma unroll
+  for (int i = 0; i < EPL; i += 2) {
+    float2 r = f2mul(cc, make_float2(acc[i], acc[i + 1]));
+    acc[i] = r.x;
+    acc[i + 1] = r.y;
+  }
+}
+
 template <int LPH>
 __device__ __forceinline__ float head_sum(float x) {
 #pragma unroll
@@ -141,10 +201,10 @@ __device__ __forceinline__ float head_sum(float x) {
 
 template <int EPL>
 __device__ __forceinline__ float dot(const float (&a)[EPL], const float (&b)[EPL]) {
-  float s = 0.f;
+  float2 s = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int i = 0; i < EPL; ++i) s = fmaf(a[i], b[i], s);
-  return s;
+  for (int i = 0; i < EPL; i += 2) s = f2fma(make_float2(a[i], a[i + 1]), make_float2(b[i], b[i + 1]), s);
+  return s.x + s.y;
 }
 
 // Source of gathered rows: index c < n_local reads the caller's tensors, c >= n_local reads a
@@ -253,16 +313,14 @@ __device__ __forceinline__ void fwd_segment(const FwdArgs& a, int64_t row, int64
       }
       const float corr = ex2(m - mx);
       l *= corr;
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+      scale_by<EPL>(corr, acc);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float p = ex2(s[u] - mx);
         l += p;
         float vf[EPL];
         to_f32<T, EPL, W>(vw[u], vf);
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) acc[i] = fmaf(p, vf[i], acc[i]);
+        axpy<EPL>(p, vf, acc);
       }
       m = mx;
     }
@@ -437,18 +495,15 @@ __device__ __forceinline__ void rowb_segment(const RowbArgs& a, int64_t row, int
         Dsum += pd;
         float kf[EPL];
         to_f32<T, EPL, W>(kw[u], kf);
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) {
-          A[i] = fmaf(pd, kf[i], A[i]);
-          Cc[i] = fmaf(p, kf[i], Cc[i]);
-        }
+        axpy<EPL>(pd, kf, A);
+        axpy<EPL>(p, kf, Cc);
       }
     }
   }
 }
 
 template <typename T, int H, int D>
-__global__ void __launch_bounds__(kBlock) rowb_kernel(RowbArgs a) {
+__global__ void __launch_bounds__(kBlock, GT_BWD_MINB) rowb_kernel(RowbArgs a) {
   using C = Cfg<T, H, D>;
   constexpr int EPL = C::EPL, W = C::W, LPH = C::LPH;
   const int lane = threadIdx.x & 31;
@@ -481,7 +536,7 @@ __global__ void __launch_bounds__(kBlock) rowb_kernel(RowbArgs a) {
     store_f32<T, EPL, W>(a.dq + row * (int64_t)(D * sizeof(T)), lane, out);
     if (lane % LPH == 0) {
       const float lse2 = (e1 == e0) ? -INFINITY : __ldg(a.lse + row * H + head) * kLog2e;
-      reinterpret_cast<float2*>(a.stats)[row * H + head] = make_float2(lse2, Ds);
+      reinterpret_cast<float2*>(a.stats + row * kSBF<H>)[head] = make_float2(lse2, Ds);
     }
   });
 }
@@ -514,7 +569,7 @@ __global__ void __launch_bounds__(kBlock) rowb_merge_kernel(MergeArgs a, const f
     for (int i = 0; i < EPL; ++i) out[i] = a.scale * fmaf(-Ds, Cc[i], A[i]);
     store_f32<T, EPL, W>(a.dq + row * (int64_t)(D * sizeof(T)), lane, out);
     if (lane % LPH == 0)
-      reinterpret_cast<float2*>(a.stats)[row * H + head] = make_float2(__ldg(lse + row * H + head) * kLog2e, Ds);
+      reinterpret_cast<float2*>(a.stats + row * kSBF<H>)[head] = make_float2(__ldg(lse + row * H + head) * kLog2e, Ds);
   }
 }
 
@@ -566,7 +621,7 @@ __device__ __forceinline__ void colb_segment(const ColbArgs& a, int64_t col, int
           a.qg.ptrs(r, pq, pg);
           ld_words<W>(pq + lane * W * 4, qw[u]);
           ld_words<W>(pg + lane * W * 4, gw[u]);
-          const float2* sp = r < nl ? reinterpret_cast<const float2*>(a.stats) + (int64_t)r * H
+          const float2* sp = r < nl ? reinterpret_cast<const float2*>(a.stats + (int64_t)r * kSBF<H>)
                                     : reinterpret_cast<const float2*>(pq + a.halo_stats_off);
           st[u] = __ldg(sp + head);
         } else {
@@ -596,18 +651,15 @@ __device__ __forceinline__ void colb_segment(const ColbArgs& a, int64_t col, int
         float qf[EPL], gf[EPL];
         to_f32<T, EPL, W>(qw[u], qf);
         to_f32<T, EPL, W>(gw[u], gf);
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) {
-          dV[i] = fmaf(p, gf[i], dV[i]);
-          dK[i] = fmaf(ds, qf[i], dK[i]);
-        }
+        axpy<EPL>(p, gf, dV);
+        axpy<EPL>(ds, qf, dK);
       }
     }
   }
 }
 
 template <typename T, int H, int D>
-__global__ void __launch_bounds__(kBlock) colb_kernel(ColbArgs a) {
+__global__ void __launch_bounds__(kBlock, GT_BWD_MINB) colb_kernel(ColbArgs a) {
   using C = Cfg<T, H, D>;
   constexpr int EPL = C::EPL, W = C::W;
   const int lane = threadIdx.x & 31;
@@ -711,7 +763,9 @@ struct Launcher {
     a.chi = ht.d_hi.as<int64_t>();
     a.cown = ht.d_owner.as<int32_t>();
     a.part = P->d_part_fwd.as<float>();
-    if (P->n_items_rows > 0) {
+    if (P->kernel == 2) {
+      GT_TRY(pipe_pass(P, 0, q, nullptr, nullptr, k, v, halo, y, nullptr, lse, st));
+    } else if (P->n_items_rows > 0) {
       GT_CUDA_TRY(cudaMemsetAsync(a.work.counter, 0, sizeof(unsigned long long), st));
       fwd_kernel<T, H, D><<<persistent_grid(fwd_kernel<T, H, D>, P->n_items_rows), kBlock, 0, st>>>(a);
     }
@@ -745,7 +799,9 @@ struct Launcher {
     a.chi = ht.d_hi.as<int64_t>();
     a.cown = ht.d_owner.as<int32_t>();
     a.part = P->d_part_rowb.as<float>();
-    if (P->n_items_rows > 0) {
+    if (P->kernel == 2) {
+      GT_TRY(pipe_pass(P, 1, q, dy, lse, k, v, halo, dq, nullptr, P->d_stats.as<float>(), st));
+    } else if (P->n_items_rows > 0) {
       GT_CUDA_TRY(cudaMemsetAsync(a.work.counter, 0, sizeof(unsigned long long), st));
       rowb_kernel<T, H, D><<<persistent_grid(rowb_kernel<T, H, D>, P->n_items_rows), kBlock, 0, st>>>(a);
     }
@@ -781,7 +837,9 @@ struct Launcher {
     a.chi = ht.d_hi.as<int64_t>();
     a.cown = ht.d_owner.as<int32_t>();
     a.part = P->d_part_colb.as<float>();
-    if (P->n_items_cols > 0) {
+    if (P->kernel == 2) {
+      GT_TRY(pipe_pass(P, 2, k, v, nullptr, q, dy, halo_in, dk, dv, nullptr, st));
+    } else if (P->n_items_cols > 0) {
       GT_CUDA_TRY(cudaMemsetAsync(a.work.counter, 0, sizeof(unsigned long long), st));
       colb_kernel<T, H, D><<<persistent_grid(colb_kernel<T, H, D>, P->n_items_cols), kBlock, 0, st>>>(a);
     }

@@ -34,8 +34,8 @@ __global__ void pack_kv_kernel(const uint4* k, const uint4* v, const int32_t* id
   }
 }
 
-__global__ void pack_in_kernel(const uint4* q, const uint4* dy, const float2* stats, const int32_t* idx,
-                               int64_t rows, int vec, int heads, int64_t row_vec, uint4* out) {
+__global__ void pack_in_kernel(const uint4* q, const uint4* dy, const uint4* stats, const int32_t* idx,
+                               int64_t rows, int vec, int svec, int64_t row_vec, uint4* out) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -46,8 +46,7 @@ __global__ void pack_in_kernel(const uint4* q, const uint4* dy, const float2* st
       o[c] = q[src * vec + c];
       o[vec + c] = dy[src * vec + c];
     }
-    float2* so = reinterpret_cast<float2*>(o + 2 * vec);
-    if (lane < heads) so[lane] = stats[src * heads + lane];
+    if (lane < svec) o[2 * vec + lane] = stats[src * svec + lane];  // (LSE2, D) block, 16-byte padded
   }
 }
 
@@ -69,8 +68,9 @@ gt_status pack_in(const void* q, const void* dy, const float* stats, const int32
   const int vec = (int)(D * elt / 16);
   const int64_t row_bytes = (2 * D * elt + 8 * heads + 15) / 16 * 16;
   int64_t blocks = std::min<int64_t>((rows + 7) / 8, 148 * 16);
-  pack_in_kernel<<<(int)blocks, 256, 0, st>>>((const uint4*)q, (const uint4*)dy, (const float2*)stats, idx, rows,
-                                               vec, heads, row_bytes / 16, (uint4*)out);
+  const int svec = (8 * heads + 15) / 16;
+  pack_in_kernel<<<(int)blocks, 256, 0, st>>>((const uint4*)q, (const uint4*)dy, (const uint4*)stats, idx, rows,
+                                               vec, svec, row_bytes / 16, (uint4*)out);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
 }

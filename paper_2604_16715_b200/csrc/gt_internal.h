@@ -99,6 +99,9 @@ struct gt_plan_s {
   gt::ChunkTable heavy_rows, heavy_cols;
   // work items in row (column) order: id >= 0 a whole row, id < 0 chunk (-1 - id) of a heavy row
   gt::DevBuf d_items_rows, d_items_cols, d_counters;
+  gt::DevBuf d_iptr_rows, d_iptr_cols;     // int64[n_items + 1]: edge range of each item
+  int kernel = 2;                          // 2 = pipelined TMA kernels (attn_pipe.cu), 1 = v1 (attn.cu)
+  int stats_stride = 0;                    // floats per row of d_stats: round16(8 heads) / 4
   int64_t n_items_rows = 0, n_items_cols = 0;
 
   // backward statistics: [n_local, heads, 2] fp32 = (LSE * log2(e), D)
@@ -152,6 +155,10 @@ bool shape_supported(int heads, int d, int dtype);
 int launches_fwd(const gt_plan_s* P);
 int launches_bwd(const gt_plan_s* P);
 
+gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b, const float* lse,
+                    const void* gather_a, const void* gather_b, const void* halo, void* out_a, void* out_b,
+                    float* out_f, cudaStream_t st);
+
 // pack kernels (comm.cu)
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,
                   void* out, cudaStream_t st);
@@ -174,4 +181,6 @@ std::vector<int32_t> send_set(int64_t n, const int64_t* row_ptr, const int32_t* 
                               int64_t blo, int64_t bhi, bool inward);
 void build_chunks(const int64_t* ptr, int64_t count, int64_t threshold, ChunkTable* t);
 std::vector<int32_t> build_items(const int64_t* ptr, int64_t count, int64_t threshold, const ChunkTable& t);
+std::vector<int64_t> build_item_ptr(const int64_t* ptr, int64_t count, const std::vector<int32_t>& items,
+                                    const ChunkTable& t);
 }  // namespace gt

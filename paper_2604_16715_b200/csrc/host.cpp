@@ -168,6 +168,14 @@ std::vector<int32_t> build_items(const int64_t* ptr, int64_t count, int64_t thre
   return items;
 }
 
+std::vector<int64_t> build_item_ptr(const int64_t* ptr, int64_t count, const std::vector<int32_t>& items,
+                                    const ChunkTable& t) {
+  std::vector<int64_t> ip(items.size() + 1);
+  for (size_t k = 0; k < items.size(); ++k) ip[k] = items[k] >= 0 ? ptr[items[k]] : t.chunk_lo[-1 - items[k]];
+  ip[items.size()] = ptr[count];
+  return ip;
+}
+
 }  // namespace gt
 
 using namespace gt;

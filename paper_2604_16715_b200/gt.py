@@ -11,7 +11,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgt.so")
+LIB_PATH = os.environ.get("GT_LIB") or os.path.join(_HERE, "libgt.so")
 
 GT_OK, GT_EINVAL, GT_EGRAPH, GT_ECONFIG, GT_ENOMEM, GT_ECUDA, GT_ENCCL, GT_ESTATE = range(8)
 STATUS_NAMES = ["GT_OK", "GT_EINVAL", "GT_EGRAPH", "GT_ECONFIG", "GT_ENOMEM", "GT_ECUDA", "GT_ENCCL", "GT_ESTATE"]
