@@ -1,23 +1,29 @@
-// Pipelined sparse-attention kernels for sm_100a: TMA bulk-copy gathers into per-warp shared-memory
-// stage rings, completion on mbarriers (UBLKCP + SYNCS in SASS).
+// Pipelined sparse-attention kernels for sm_100a: asynchronous gathers (cp.async / LDGSTS) of
+// neighbour rows into per-warp shared-memory stage rings.
 //
-// Same mathematics as attn.cu (Eq. 2/4/5 and Section 2.2):
+// Same mathematics as the reference kernels in attn.cu (Eq. 2/4/5, Section 2.2):
 //   pass 0 (fwd):  per row i:    s_e = scale <q_i,k_j>, online softmax, y_i = sum p_e v_j / l, LSE
 //   pass 1 (rowb): per row i:    p_e = exp(s_e - LSE_i), dP_e = <dY_i, v_j>, D_i = sum p dP,
 //                                dQ_i = scale (sum p dP k_j - D_i sum p k_j)
 //   pass 2 (colb): per column j: p_e, dP_e recomputed from (q_i, dY_i, LSE_i, D_i);
 //                                dV_j = sum p dY_i, dK_j = scale sum p (dP - D_i) q_i
 //
-// Execution model.  Persistent CTAs of kWarps warps; every warp owns a ring of S stages in shared
-// memory, each stage holding up to U gathered neighbours (2 rows of D*sizeof(T) bytes each, plus the
-// neighbour's (LSE, D) block in pass 2) and an "own" slot with the row/column's own data.  The warp
-// grabs batches of G consecutive work items (rows, or chunks of heavy rows, in row order) with one
-// atomicAdd; because items are consecutive their edge ranges form one contiguous span of the
-// neighbour array, streamed through a 32-entry register window.  The warp is its own producer: lane u
-// issues cp.async.bulk copies of neighbour u's rows straight from global memory into the stage
-// (one instruction per 512-byte row) and lane 0 posts the byte count on the stage's mbarrier; then
-// the warp consumes the oldest stage (LDS of the lane's 16-byte slice) and refills it.  S*U
-// neighbours (16 KB) are in flight per warp without holding registers, across row boundaries.
+// Execution model.  Persistent CTAs; every warp owns a ring of kS stages in shared memory, each
+// holding up to U neighbours (two feature rows, plus the neighbour's (LSE2, D) pair in pass 2), and
+// an "own" slot per stage for the data of the row (column) an item starts.  Warps grab batches of
+// kG consecutive work items (rows, or chunks of heavy rows, in row order) with one atomicAdd, so the
+// resident warps sweep the graph in a narrow window of rows and the neighbours they gather stay in
+// L2 (community locality); consecutive items have contiguous edge ranges, streamed through a
+// 32-entry register window of neighbour ids with the next window prefetched.
+//
+// The warp is its own producer.  Lane l issues cp.async copies of ITS 16-byte slice of every
+// gathered row (a whole 512-byte row is one coalesced request per warp) and later reads back only
+// those same bytes, so completion needs no barrier or cross-lane synchronisation: one
+// cp.async.commit_group per stage and cp.async.wait_group(kS - 1) before consuming the oldest
+// stage.  kS * U neighbours (16 KB at D = 256 bf16) stay in flight per warp, across row boundaries,
+// without occupying registers.  (A TMA cp.async.bulk variant - one lane issuing whole-row copies on
+// an mbarrier - was measured 2x slower: the per-lane UBLKCP issue loop and barrier traffic made it
+// instruction bound.)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -33,9 +39,18 @@ namespace pipe {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kWarps = 4;     // warps per CTA
-constexpr int kS = 4;         // stages per warp
-constexpr int kG = 4;         // items per grab
+#ifndef GT_PIPE_WARPS
+#define GT_PIPE_WARPS 4
+#endif
+#ifndef GT_PIPE_STAGES
+#define GT_PIPE_STAGES 2
+#endif
+#ifndef GT_PIPE_GRAB
+#define GT_PIPE_GRAB 4
+#endif
+constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
+constexpr int kS = GT_PIPE_STAGES;      // stages per warp (2 measured best: more resident warps)
+constexpr int kG = GT_PIPE_GRAB;        // items per grab
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -45,29 +60,26 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ __forceinline__ void bar_init(void* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(1));
-}
-__device__ __forceinline__ void bar_expect(void* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bar_wait(void* bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
-        : "=r"(done)
-        : "r"(su32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, void* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
+// 16-byte copy that zero-fills the destination instead of reading when !valid (no branch)
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 16 : 0)
                : "memory");
 }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cp_async8z(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(su32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
   float2 d;
@@ -83,17 +95,16 @@ template <typename T, int H, int D, int PASS>
 struct PC {
   static constexpr int RB = D * (int)sizeof(T);          // bytes of one feature row
   static constexpr int EPL = D / 32;                      // elements per lane
-  static constexpr int LB = EPL * (int)sizeof(T);         // bytes per lane of one row
-  static constexpr int W = LB / 4;                        // 32-bit words per lane
+  static constexpr int LB = EPL * (int)sizeof(T);         // bytes per lane of one row (8..64)
   static constexpr int LPH = 32 / H;                      // lanes per head
-  static constexpr int SB = (8 * H + 15) / 16 * 16;       // (LSE2, D) block per row, 16-byte padded
-  static constexpr int LSEB = (4 * H + 15) / 16 * 16;     // lse block copied for the own row (pass 1)
-  static constexpr int EB = 2 * RB + (PASS == 2 ? SB : 0);                        // bytes per neighbour
-  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? 2 * RB + LSEB : 2 * RB);
+  static constexpr int SB = (8 * H + 15) / 16 * 16;       // (LSE2, D) row of the stats array, padded
+  static constexpr int EB = (2 * RB + (PASS == 2 ? 8 * H : 0) + 15) / 16 * 16;    // bytes per neighbour
+  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? 2 * RB + 4 * H : 2 * RB);
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
-  static constexpr int STAGE = U * EB;
-  static constexpr int WARP_SMEM = kS * (STAGE + OWN) + kS * 16 + kS * 8;
-  static_assert(W == 2 || W % 4 == 0, "lane slice must be 8 bytes or a multiple of 16");
+  static constexpr int STAGE = (U * EB + 15) / 16 * 16;
+  static constexpr int OWNP = (OWN + 15) / 16 * 16;
+  static constexpr int WARP_SMEM = kS * (STAGE + OWNP);
+  static_assert(LB == 8 || LB % 16 == 0, "lane slice must be 8 bytes or a multiple of 16");
 };
 
 struct PArgs {
@@ -105,7 +116,7 @@ struct PArgs {
   unsigned long long* counter;
   const char* ga;        // local tensor gathered first  (k | k | q)
   const char* gb;        // local tensor gathered second (v | v | dy)
-  const char* gs;        // local (LSE2, D) blocks [n_local][SB] (pass 2)
+  const char* gs;        // local (LSE2, D) rows [n_local][SB bytes] (pass 2)
   const char* halo;      // packed remote rows
   int64_t halo_stride;
   int64_t n_local;
@@ -119,15 +130,32 @@ struct PArgs {
   float qscale, scale;
 };
 
-struct Meta {
-  int32_t own;           // item id (row/col) or chunk (-1 - c)
-  int16_t cnt;
-  int8_t first, last;
-  int32_t slot, pad;
-};
+// lane slice copy of one row: LB bytes at byte offset lane * LB
+template <int LB>
+__device__ __forceinline__ void cp_slice(char* dst_row, const char* src_row, int lane) {
+  if constexpr (LB == 8) {
+    cp_async<8>(dst_row + lane * 8, src_row + lane * 8);
+  } else {
+#pragma unroll
+    for (int i = 0; i < LB / 16; ++i) cp_async<16>(dst_row + lane * LB + 16 * i, src_row + lane * LB + 16 * i);
+  }
+}
 
-template <int W>
-__device__ __forceinline__ void lds_words(const char* p, uint32_t (&w)[W]) {
+template <int LB>
+__device__ __forceinline__ void cp_slice_z(char* dst_row, const char* src_row, int lane, bool valid) {
+  if constexpr (LB == 8) {
+    cp_async8z(dst_row + lane * 8, src_row + lane * 8, valid);
+  } else {
+#pragma unroll
+    for (int i = 0; i < LB / 16; ++i)
+      cp_async16z(dst_row + lane * LB + 16 * i, src_row + lane * LB + 16 * i, valid);
+  }
+}
+
+template <typename T, int EPL>
+__device__ __forceinline__ void lds_f32(const char* p, float (&f)[EPL]) {
+  constexpr int W = EPL * (int)sizeof(T) / 4;
+  uint32_t w[W];
   if constexpr (W % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < W / 4; ++i) {
@@ -138,10 +166,6 @@ __device__ __forceinline__ void lds_words(const char* p, uint32_t (&w)[W]) {
     uint2 x = *reinterpret_cast<const uint2*>(p);
     w[0] = x.x; w[1] = x.y;
   }
-}
-
-template <typename T, int EPL, int W>
-__device__ __forceinline__ void to_f32(const uint32_t (&w)[W], float (&f)[EPL]) {
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
     for (int i = 0; i < EPL; ++i) f[i] = __uint_as_float(w[i]);
@@ -152,14 +176,6 @@ __device__ __forceinline__ void to_f32(const uint32_t (&w)[W], float (&f)[EPL]) 
       f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
     }
   }
-}
-
-template <typename T, int EPL>
-__device__ __forceinline__ void lds_f32(const char* p, float (&f)[EPL]) {
-  constexpr int W = EPL * (int)sizeof(T) / 4;
-  uint32_t w[W];
-  lds_words<W>(p, w);
-  to_f32<T, EPL, W>(w, f);
 }
 
 template <typename T, int EPL>
@@ -204,6 +220,17 @@ __device__ __forceinline__ void axpy(float p, const float (&x)[EPL], float (&acc
   }
 }
 
+template <int EPL>
+__device__ __forceinline__ void scale2(float c, float (&acc)[EPL]) {
+  const float2 cc = make_float2(c, c);
+#pragma unroll
+  for (int i = 0; i < EPL; i += 2) {
+    float2 r = f2fma(cc, make_float2(acc[i], acc[i + 1]), make_float2(0.f, 0.f));
+    acc[i] = r.x;
+    acc[i + 1] = r.y;
+  }
+}
+
 template <int LPH>
 __device__ __forceinline__ float head_sum(float x) {
 #pragma unroll
@@ -211,59 +238,57 @@ __device__ __forceinline__ float head_sum(float x) {
   return x;
 }
 
+struct Meta {      // warp-uniform description of one filled stage
+  int32_t own;     // row/column id, or chunk -1 - c
+  int32_t cnt;     // neighbours in the stage (0 = no work left)
+  bool first, last;
+};
+
 // ------------------------------------------------------------------ kernel --
-template <typename T, int H, int D, int PASS>
+template <typename T, int H, int D, int PASS, bool HALO>
 __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
   using C = PC<T, H, D, PASS>;
-  constexpr int EPL = C::EPL, LPH = C::LPH, RB = C::RB, EB = C::EB, U = C::U;
+  constexpr int EPL = C::EPL, LPH = C::LPH, RB = C::RB, EB = C::EB, U = C::U, LB = C::LB;
   extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int head = lane / LPH;
-  char* wbase = smem + (size_t)wid * C::WARP_SMEM;
-  char* stages = wbase;                                   // kS * STAGE
-  char* owns = stages + kS * C::STAGE;                    // kS * OWN
-  Meta* meta = reinterpret_cast<Meta*>(owns + kS * C::OWN);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(meta) + kS * 16);
-  if (lane == 0)
-    for (int s = 0; s < kS; ++s) bar_init(&bars[s]);
-  __syncwarp();
-  fence_async_smem();
+  char* const stages = smem + (size_t)wid * C::WARP_SMEM;   // kS * STAGE
+  char* const owns = stages + kS * C::STAGE;                 // kS * OWNP
 
-  // ---------------- producer state (warp-uniform except lane-distributed tables) ----------------
-  int64_t t_next = 0, t_end = 0;     // items of the current batch not yet started
-  int64_t my_ptr = 0;                // lane k (< kG): iptr[t0 + k]; lane kG: iptr[t0 + kG] (batch end)
-  int32_t my_own = 0;                // lane k: iown[t0 + k]
-  int64_t batch_t0 = 0;
+  // ---------------- producer state (warp-uniform; per-lane only the tables) ----------------
+  int64_t t_next = 0, t_end = 0, batch_t0 = 0, batch_e1 = 0;
+  int64_t my_ptr = 0;                // lane k <= kG: iptr[batch_t0 + k]
+  int32_t my_own = 0;                // lane k < kG: iown[batch_t0 + k]
   bool done = false;
   int64_t pe = 0, pe_end = 0;        // current item's remaining edge range
   int32_t cur_own = 0;
-  int cur_first = 0;
-  int64_t win_base = 0;              // neighbour window: lane l holds nbr[win_base + l]
-  int32_t win = 0;
-  int32_t item_seq = 0;
-  int64_t batch_e1 = 0;
+  bool cur_first = false;
+  int64_t win_base = 0;              // lane l holds nbr[win_base + l] in win, nbr[win_base + 32 + l] in win_next
+  int32_t win = 0, win_next = 0;
 
-  auto finalize_empty = [&](int32_t own) {
-    // rows with no entries: Y = 0, LSE = -inf / dQ = 0, stats (-inf, 0) / dK = dV = 0
+  auto finalize_empty = [&](int64_t r) {  // a row (column) with no entries
     float z[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; ++i) z[i] = 0.f;
-    const int64_t r = own;
+    stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, z);
     if constexpr (PASS == 0) {
-      stg_f32<T, EPL>(a.out_a + r * RB + lane * C::LB, z);
       if (lane % LPH == 0) a.out_f[r * H + head] = -INFINITY;
     } else if constexpr (PASS == 1) {
-      stg_f32<T, EPL>(a.out_a + r * RB + lane * C::LB, z);
       if (lane % LPH == 0)
         reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(-INFINITY, 0.f);
     } else {
-      stg_f32<T, EPL>(a.out_a + r * RB + lane * C::LB, z);
-      stg_f32<T, EPL>(a.out_b + r * RB + lane * C::LB, z);
+      stg_f32<T, EPL>(a.out_b + r * RB + lane * LB, z);
     }
   };
 
-  // Advances to the next non-empty item; returns false when the grid's work is exhausted.
+  auto load_window = [&](int64_t base) {
+    win_base = base;
+    win = (base + lane < batch_e1) ? __ldg(a.nbr + base + lane) : 0;
+    win_next = (base + 32 + lane < batch_e1) ? __ldg(a.nbr + base + 32 + lane) : 0;
+  };
+
+  // Advances to the next non-empty item; false when the grid's work is exhausted.
   auto next_item = [&]() -> bool {
     for (;;) {
       if (t_next >= t_end) {
@@ -282,7 +307,7 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
         my_ptr = (lane <= kG && k <= a.nitems) ? __ldg(a.iptr + k) : 0;
         my_own = (lane < kG && k < a.nitems) ? __ldg(a.iown + k) : 0;
         batch_e1 = __shfl_sync(kFull, my_ptr, (int)(t_end - batch_t0));
-        win_base = -1000000000000ll;
+        load_window(__shfl_sync(kFull, my_ptr, 0));
       }
       const int k = (int)(t_next - batch_t0);
       const int64_t e0 = __shfl_sync(kFull, my_ptr, k);
@@ -296,236 +321,214 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
       pe = e0;
       pe_end = e1;
       cur_own = own;
-      cur_first = 1;
+      cur_first = true;
       return true;
     }
   };
 
-  // Fills stage `s` with the next group of neighbours; returns false if no work is left.
-  auto produce = [&](int s) -> bool {
-    if (pe >= pe_end && !next_item()) return false;
-    if (pe < win_base || pe >= win_base + 32) {
-      win_base = pe;
-      win = (pe + lane < batch_e1) ? __ldg(a.nbr + pe + lane) : 0;
+  // Fills stage `s` with the next group of neighbours (this lane's slices) and returns its meta.
+  auto produce = [&](int s) -> Meta {
+    Meta md;
+    md.cnt = 0;
+    md.own = 0;
+    md.first = md.last = false;
+    if (pe >= pe_end && !next_item()) return md;
+    if (pe >= win_base + 32) {  // slide the neighbour window; prefetch the one after
+      win_base += 32;
+      win = win_next;
+      win_next = (win_base + 32 + lane < batch_e1) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
     }
     int64_t lim = pe_end - pe;
     if (win_base + 32 - pe < lim) lim = win_base + 32 - pe;
     const int cnt = lim < U ? (int)lim : U;
-    const int slot = item_seq % kS;
-    const bool first = cur_first != 0;
-    const bool last = pe + cnt == pe_end;
-    if (lane == 0) {
-      Meta m;
-      m.own = cur_own;
-      m.cnt = (int16_t)cnt;
-      m.first = first;
-      m.last = last;
-      m.slot = slot;
-      m.pad = 0;
-      meta[s] = m;
-      uint32_t bytes = (uint32_t)(cnt * (2 * RB + (PASS == 2 ? C::SB : 0)));
-      if (first) bytes += (uint32_t)(PASS == 0 ? RB : (PASS == 1 ? 2 * RB + C::LSEB : 2 * RB));
-      bar_expect(&bars[s], bytes);
-    }
-    __syncwarp();
-    fence_async_smem();
-    const int32_t c = __shfl_sync(kFull, win, (int)((pe - win_base + lane) & 31));
     char* st = stages + s * C::STAGE;
-    if (lane < cnt) {
+    const int off = (int)(pe - win_base);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // branch-free: neighbours u >= cnt are zero-filled, not read
+      const bool valid = u < cnt;
+      const int64_t ci = __shfl_sync(kFull, win, (off + u) & 31);
+      const int64_t cv = valid ? ci : 0;
       const char *pa, *pb, *ps = nullptr;
-      const int64_t ci = c;
-      if (ci < a.n_local) {
-        pa = a.ga + ci * RB;
-        pb = a.gb + ci * RB;
-        if constexpr (PASS == 2) ps = a.gs + ci * C::SB;
+      if constexpr (HALO) {
+        const bool loc = cv < a.n_local;
+        const char* hrow = a.halo + (cv - a.n_local) * a.halo_stride;
+        pa = loc ? a.ga + cv * RB : hrow;
+        pb = loc ? a.gb + cv * RB : hrow + RB;
+        if constexpr (PASS == 2) ps = loc ? a.gs + cv * C::SB : hrow + 2 * RB;
       } else {
-        pa = a.halo + (ci - a.n_local) * a.halo_stride;
-        pb = pa + RB;
-        if constexpr (PASS == 2) ps = pa + 2 * RB;
+        pa = a.ga + cv * RB;
+        pb = a.gb + cv * RB;
+        if constexpr (PASS == 2) ps = a.gs + cv * C::SB;
       }
-      char* dst = st + lane * EB;
-      bulk_g2s(dst, pa, RB, &bars[s]);
-      bulk_g2s(dst + RB, pb, RB, &bars[s]);
-      if constexpr (PASS == 2) bulk_g2s(dst + 2 * RB, ps, C::SB, &bars[s]);
+      char* dst = st + u * EB;
+      cp_slice_z<LB>(dst, pa, lane, valid);
+      cp_slice_z<LB>(dst + RB, pb, lane, valid);
+      if constexpr (PASS == 2) cp_async8z(dst + 2 * RB + head * 8, ps + head * 8, valid);
     }
-    if (first) {
-      char* o = owns + slot * C::OWN;
+    md.cnt = cnt;
+    md.own = cur_own;
+    md.first = cur_first;
+    md.last = pe + cnt == pe_end;
+    if (cur_first) {
+      char* o = owns + s * C::OWNP;
       const int64_t r = cur_own >= 0 ? cur_own : a.cown[-1 - (int64_t)cur_own];
-      if (lane == 0) bulk_g2s(o, a.oa + r * RB, RB, &bars[s]);
-      if constexpr (PASS >= 1) {
-        if (lane == 1) bulk_g2s(o + RB, a.ob + r * RB, RB, &bars[s]);
-      }
-      if constexpr (PASS == 1) {
-        if (lane == 2) {
-          const char* lp = reinterpret_cast<const char*>(a.lse) + r * H * 4;
-          bulk_g2s(o + 2 * RB, reinterpret_cast<const char*>((uintptr_t)lp & ~(uintptr_t)15), C::LSEB, &bars[s]);
-        }
-      }
-      ++item_seq;
-      cur_first = 0;
+      cp_slice<LB>(o, a.oa + r * RB, lane);
+      if constexpr (PASS >= 1) cp_slice<LB>(o + RB, a.ob + r * RB, lane);
+      if constexpr (PASS == 1) cp_async<4>(o + 2 * RB + head * 4, a.lse + r * H + head);
+      cur_first = false;
     }
     pe += cnt;
-    return true;
+    return md;
   };
 
   // ---------------- consumer state ----------------
   float q[EPL], g[EPL], acc[EPL], acc2[EPL];
-  float m = 0.f, l = 0.f, aux = 0.f;   // fwd: running max / sum; rowb: lse2 (m), D (l)
+  float m = 0.f, l = 0.f;   // fwd: running max / sum (base 2); rowb: lse2 (m), D (l)
 
-  int issued = 0;
+  Meta md[kS];
+#pragma unroll
   for (int s = 0; s < kS; ++s) {
-    if (!produce(s)) break;
-    ++issued;
+    md[s] = produce(s);
+    cp_commit();
   }
-  for (int c = 0; c < issued; ++c) {
-    const int s = c % kS;
-    bar_wait(&bars[s], (uint32_t)((c / kS) & 1));
-    const Meta md = meta[s];
-    const char* st = stages + s * C::STAGE;
-    if (md.first) {
-      const char* o = owns + md.slot * C::OWN;
-      if constexpr (PASS == 0) {
-        lds_f32<T, EPL>(o + lane * C::LB, q);
+  for (;;) {
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; }
-        m = -INFINITY;
-        l = 0.f;
-      } else if constexpr (PASS == 1) {
-        lds_f32<T, EPL>(o + lane * C::LB, q);
-        lds_f32<T, EPL>(o + RB + lane * C::LB, g);
-        const int64_t r = md.own >= 0 ? md.own : a.cown[-1 - (int64_t)md.own];
-        const int off = (H * 4 >= 16) ? 0 : (int)((r * H * 4) & 15);
-        m = reinterpret_cast<const float*>(o + 2 * RB + off)[head] * kLog2e;
+    for (int s = 0; s < kS; ++s) {
+      cp_wait<kS - 1>();
+      const Meta cur = md[s];
+      if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one
+      const char* st = stages + s * C::STAGE;
+      if (cur.first) {
+        const char* o = owns + s * C::OWNP;
+        if constexpr (PASS == 0) {
+          lds_f32<T, EPL>(o + lane * LB, q);
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
-        l = 0.f;
-      } else {
-        lds_f32<T, EPL>(o + lane * C::LB, q);      // k_j
-        lds_f32<T, EPL>(o + RB + lane * C::LB, g); // v_j
+          for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; }
+          m = -INFINITY;
+          l = 0.f;
+        } else if constexpr (PASS == 1) {
+          lds_f32<T, EPL>(o + lane * LB, q);
+          lds_f32<T, EPL>(o + RB + lane * LB, g);
+          m = reinterpret_cast<const float*>(o + 2 * RB)[head] * kLog2e;
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
-      }
-    }
-    const int cnt = md.cnt;
-    if constexpr (PASS == 0) {
-      float sc[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < cnt) {
-          float kf[EPL];
-          lds_f32<T, EPL>(st + u * EB + lane * C::LB, kf);
-          sc[u] = head_sum<LPH>(dot<EPL>(q, kf));
+          for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
+          l = 0.f;
         } else {
-          sc[u] = -INFINITY;
+          lds_f32<T, EPL>(o + lane * LB, q);      // k_j
+          lds_f32<T, EPL>(o + RB + lane * LB, g); // v_j
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
         }
       }
-      float mx = m;
+      const int cnt = cur.cnt;
+      if constexpr (PASS == 0) {
+        float sc[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) mx = fmaxf(mx, sc[u]);
-      const float corr = ex2(m - mx);
-      l *= corr;
+        for (int u = 0; u < U; ++u) {
+          float kf[EPL];
+          lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
+          const float sv = head_sum<LPH>(dot<EPL>(q, kf));
+          sc[u] = u < cnt ? sv : -INFINITY;
+        }
+        float mx = m;
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] *= corr;
+        for (int u = 0; u < U; ++u) mx = fmaxf(mx, sc[u]);
+        const float corr = ex2(m - mx);
+        l *= corr;
+        scale2<EPL>(corr, acc);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < cnt) {
-          const float p = ex2(sc[u] - mx);
+        for (int u = 0; u < U; ++u) {
+          const float p = ex2(sc[u] - mx);  // 0 for masked neighbours
           l += p;
           float vf[EPL];
-          lds_f32<T, EPL>(st + u * EB + RB + lane * C::LB, vf);
+          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
           axpy<EPL>(p, vf, acc);
         }
-      }
-      m = mx;
-    } else if constexpr (PASS == 1) {
+        m = mx;
+      } else if constexpr (PASS == 1) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < cnt) {
+        for (int u = 0; u < U; ++u) {
           float kf[EPL], vf[EPL];
-          lds_f32<T, EPL>(st + u * EB + lane * C::LB, kf);
-          lds_f32<T, EPL>(st + u * EB + RB + lane * C::LB, vf);
+          lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
+          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
           const float s_ = head_sum<LPH>(dot<EPL>(q, kf));
           const float dp = head_sum<LPH>(dot<EPL>(g, vf));
-          const float p = ex2(s_ - m);
+          const float p = u < cnt ? ex2(s_ - m) : 0.f;
           const float pd = p * dp;
           l += pd;
           axpy<EPL>(pd, kf, acc);
           axpy<EPL>(p, kf, acc2);
         }
-      }
-    } else {
+      } else {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < cnt) {
+        for (int u = 0; u < U; ++u) {
           float qf[EPL], gf[EPL];
-          lds_f32<T, EPL>(st + u * EB + lane * C::LB, qf);
-          lds_f32<T, EPL>(st + u * EB + RB + lane * C::LB, gf);
+          lds_f32<T, EPL>(st + u * EB + lane * LB, qf);
+          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, gf);
           const float2 sd = reinterpret_cast<const float2*>(st + u * EB + 2 * RB)[head];
           const float s_ = head_sum<LPH>(dot<EPL>(qf, q));
           const float dp = head_sum<LPH>(dot<EPL>(gf, g));
-          const float p = ex2(s_ - sd.x);
+          const float p = u < cnt ? ex2(s_ - sd.x) : 0.f;
           const float ds = p * (dp - sd.y);
           axpy<EPL>(p, gf, acc2);   // dV
           axpy<EPL>(ds, qf, acc);   // dK (unscaled)
         }
       }
-    }
-    if (md.last) {
-      const int32_t own = md.own;
-      if (own < 0) {  // chunk of a heavy row/column: partial state
-        const int64_t ch = -1 - (int64_t)own;
-        if constexpr (PASS == 0) {
-          float* pp = a.part + ch * (int64_t)(D + 2 * H);
+      if (cur.last) {
+        const int32_t own = cur.own;
+        if (own < 0) {  // chunk of a heavy row/column: partial state for the merge kernel
+          const int64_t ch = -1 - (int64_t)own;
+          if constexpr (PASS == 0) {
+            float* pp = a.part + ch * (int64_t)(D + 2 * H);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
-          if (lane % LPH == 0) { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
-        } else if constexpr (PASS == 1) {
-          float* pp = a.part + ch * (int64_t)(2 * D + H);
+            for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
+            if (lane % LPH == 0) { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
+          } else if constexpr (PASS == 1) {
+            float* pp = a.part + ch * (int64_t)(2 * D + H);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
-          if (lane % LPH == 0) pp[2 * D + head] = l;
+            for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
+            if (lane % LPH == 0) pp[2 * D + head] = l;
+          } else {
+            float* pp = a.part + ch * (int64_t)(2 * D);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
+          }
         } else {
-          float* pp = a.part + ch * (int64_t)(2 * D);
+          const int64_t r = own;
+          if constexpr (PASS == 0) {
+            const float inv = 1.f / l;
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
-        }
-      } else {
-        const int64_t r = own;
-        if constexpr (PASS == 0) {
-          const float inv = 1.f / l;
+            for (int i = 0; i < EPL; ++i) acc[i] *= inv;
+            stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
+            if (lane % LPH == 0) a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
+          } else if constexpr (PASS == 1) {
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] *= inv;
-          stg_f32<T, EPL>(a.out_a + r * RB + lane * C::LB, acc);
-          if (lane % LPH == 0) a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
-        } else if constexpr (PASS == 1) {
+            for (int i = 0; i < EPL; ++i) acc[i] = a.scale * fmaf(-l, acc2[i], acc[i]);
+            stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
+            if (lane % LPH == 0)
+              reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(m, l);
+          } else {
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] = a.scale * fmaf(-l, acc2[i], acc[i]);
-          stg_f32<T, EPL>(a.out_a + r * RB + lane * C::LB, acc);
-          if (lane % LPH == 0)
-            reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(m, l);
-        } else {
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) acc[i] *= a.scale;
-          stg_f32<T, EPL>(a.out_a + r * RB + lane * C::LB, acc);
-          stg_f32<T, EPL>(a.out_b + r * RB + lane * C::LB, acc2);
+            for (int i = 0; i < EPL; ++i) acc[i] *= a.scale;
+            stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
+            stg_f32<T, EPL>(a.out_b + r * RB + lane * LB, acc2);
+          }
         }
       }
+      md[s] = produce(s);   // refill the stage just consumed (this lane's own slices only)
+      cp_commit();
     }
-    __syncwarp();
-    if (produce(s)) ++issued;
   }
-  // every issued stage was consumed; produce() returned false only once the work was exhausted
-  // (next_item() finalised any empty rows on the way)
 }
 
 // ----------------------------------------------------------------- launcher --
-template <typename T, int H, int D, int PASS>
+template <typename T, int H, int D, int PASS, bool HALO>
 gt_status launch(const PArgs& a, cudaStream_t st) {
   using C = PC<T, H, D, PASS>;
   static int grid = 0;
   const size_t smem = (size_t)kWarps * C::WARP_SMEM;
   if (!grid) {
-    auto k = pipe_kernel<T, H, D, PASS>;
+    auto k = pipe_kernel<T, H, D, PASS, HALO>;
     GT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
@@ -537,7 +540,7 @@ gt_status launch(const PArgs& a, cudaStream_t st) {
   const int64_t want = (a.nitems + kG - 1) / kG;
   const int g = (int)std::min<int64_t>(grid, (want + kWarps - 1) / kWarps);
   GT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
-  pipe_kernel<T, H, D, PASS><<<g, kWarps * 32, smem, st>>>(a);
+  pipe_kernel<T, H, D, PASS, HALO><<<g, kWarps * 32, smem, st>>>(a);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
 }
@@ -545,9 +548,14 @@ gt_status launch(const PArgs& a, cudaStream_t st) {
 template <typename T, int H, int D>
 struct Ops {
   static gt_status run(int pass, const PArgs& a, cudaStream_t st) {
-    if (pass == 0) return launch<T, H, D, 0>(a, st);
-    if (pass == 1) return launch<T, H, D, 1>(a, st);
-    return launch<T, H, D, 2>(a, st);
+    if (a.halo) {
+      if (pass == 0) return launch<T, H, D, 0, true>(a, st);
+      if (pass == 1) return launch<T, H, D, 1, true>(a, st);
+      return launch<T, H, D, 2, true>(a, st);
+    }
+    if (pass == 0) return launch<T, H, D, 0, false>(a, st);
+    if (pass == 1) return launch<T, H, D, 1, false>(a, st);
+    return launch<T, H, D, 2, false>(a, st);
   }
 };
 
@@ -567,7 +575,7 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
 
 }  // namespace pipe
 
-// Entry points used by launch_* in attn.cu when the pipelined kernels are selected.
+// Runs one pass with the pipelined kernel (merges of chunked rows are launched by the caller).
 gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b, const float* lse,
                     const void* gather_a, const void* gather_b, const void* halo, void* out_a, void* out_b,
                     float* out_f, cudaStream_t st) {
