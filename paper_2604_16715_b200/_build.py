@@ -45,8 +45,12 @@ def _compile(src: str, verbose: bool, defines=(), objdir=OBJ) -> str:
 
 def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, objdir: str = OBJ) -> str:
     """Compiles csrc/ into `lib`; `defines` (e.g. ["GT_FFMA2=0"]) build tuning variants."""
-    os.makedirs(objdir, exist_ok=True)
     srcs = sources()
+    deps = srcs + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
+    deps.append(os.path.join(HERE, "..", "include", "gt.h"))
+    if not force and not defines and not _stale(lib, deps):
+        return lib  # up to date (object files need not exist, e.g. on a fresh GPU box)
+    os.makedirs(objdir, exist_ok=True)
     if force:
         for f in os.listdir(objdir):
             os.remove(os.path.join(objdir, f))
