@@ -98,7 +98,7 @@ struct PC {
   static constexpr int LB = EPL * (int)sizeof(T);         // bytes per lane of one row (8..64)
   static constexpr int LPH = 32 / H;                      // lanes per head
   static constexpr int SB = (8 * H + 15) / 16 * 16;       // (LSE2, D) row of the stats array, padded
-  static constexpr int EB = (2 * RB + (PASS == 2 ? 8 * H : 0) + 15) / 16 * 16;    // bytes per neighbour
+  static constexpr int EB = 2 * RB + (PASS == 2 ? SB : 0);                          // bytes per neighbour
   static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? 2 * RB + 4 * H : 2 * RB);
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
   static constexpr int STAGE = (U * EB + 15) / 16 * 16;
@@ -228,6 +228,51 @@ __device__ __forceinline__ void scale2(float c, float (&acc)[EPL]) {
     float2 r = f2fma(cc, make_float2(acc[i], acc[i + 1]), make_float2(0.f, 0.f));
     acc[i] = r.x;
     acc[i + 1] = r.y;
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void lds_raw(const char* p, uint32_t (&w)[W]) {
+  if constexpr (W % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < W / 4; ++i) {
+      uint4 x = *reinterpret_cast<const uint4*>(p + 16 * i);
+      w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
+    }
+  } else {
+    uint2 x = *reinterpret_cast<const uint2*>(p);
+    w[0] = x.x; w[1] = x.y;
+  }
+}
+
+__device__ __forceinline__ float fma_bf16(uint16_t a, uint16_t b, float c) {
+  float d;
+  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+
+// <a, b> of two rows held as raw storage words, accumulated in fp32.  bf16: FHFMA.BF16 reads the
+// two halves of each word in place (exact products, fp32 sums) - no unpacking.
+template <typename T, int W>
+__device__ __forceinline__ float dot_raw(const uint32_t (&a)[W], const uint32_t (&b)[W]) {
+  if constexpr (sizeof(T) == 2) {
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      uint16_t al, ah, bl, bh;
+      asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a[i]));
+      asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b[i]));
+      s0 = fma_bf16(al, bl, s0);
+      s1 = fma_bf16(ah, bh, s1);
+    }
+    return s0 + s1;
+  } else {
+    float2 s = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < W; i += 2)
+      s = f2fma(make_float2(__uint_as_float(a[i]), __uint_as_float(a[i + 1])),
+                make_float2(__uint_as_float(b[i]), __uint_as_float(b[i + 1])), s);
+    return s.x + s.y;
   }
 }
 
@@ -363,7 +408,11 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
       char* dst = st + u * EB;
       cp_slice_z<LB>(dst, pa, lane, valid);
       cp_slice_z<LB>(dst + RB, pb, lane, valid);
-      if constexpr (PASS == 2) cp_async8z(dst + 2 * RB + head * 8, ps + head * 8, valid);
+      // (LSE2, D) block of the neighbour: SB / 16 lanes copy 16 bytes each (read by all lanes of a head
+      // after the stage's wait + __syncwarp)
+      if constexpr (PASS == 2) {
+        if (lane < C::SB / 16) cp_async16z(dst + 2 * RB + lane * 16, ps + lane * 16, valid);
+      }
     }
     md.cnt = cnt;
     md.own = cur_own;
@@ -382,7 +431,9 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
   };
 
   // ---------------- consumer state ----------------
+  constexpr int W = LB / 4;
   float q[EPL], g[EPL], acc[EPL], acc2[EPL];
+  uint32_t ow[W];           // raw own-row words: q (fwd) or dY (rowb), dotted with FHFMA / FFMA2
   float m = 0.f, l = 0.f;   // fwd: running max / sum (base 2); rowb: lse2 (m), D (l)
 
   Meta md[kS];
@@ -395,20 +446,21 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
       cp_wait<kS - 1>();
+      if constexpr (PASS == 2) __syncwarp();  // stats blocks were copied by other lanes
       const Meta cur = md[s];
       if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one
       const char* st = stages + s * C::STAGE;
       if (cur.first) {
         const char* o = owns + s * C::OWNP;
         if constexpr (PASS == 0) {
-          lds_f32<T, EPL>(o + lane * LB, q);
+          lds_raw<W>(o + lane * LB, ow);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; }
+          for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
           m = -INFINITY;
           l = 0.f;
         } else if constexpr (PASS == 1) {
           lds_f32<T, EPL>(o + lane * LB, q);
-          lds_f32<T, EPL>(o + RB + lane * LB, g);
+          lds_raw<W>(o + RB + lane * LB, ow);
           m = reinterpret_cast<const float*>(o + 2 * RB)[head] * kLog2e;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
@@ -425,9 +477,9 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
         float sc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          float kf[EPL];
-          lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
-          const float sv = head_sum<LPH>(dot<EPL>(q, kf));
+          uint32_t kw[W];
+          lds_raw<W>(st + u * EB + lane * LB, kw);
+          const float sv = head_sum<LPH>(dot_raw<T, W>(ow, kw)) * a.qscale;
           sc[u] = u < cnt ? sv : -INFINITY;
         }
         float mx = m;
@@ -448,11 +500,12 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
       } else if constexpr (PASS == 1) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          float kf[EPL], vf[EPL];
+          float kf[EPL];
+          uint32_t vw[W];
           lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
-          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
+          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
           const float s_ = head_sum<LPH>(dot<EPL>(q, kf));
-          const float dp = head_sum<LPH>(dot<EPL>(g, vf));
+          const float dp = head_sum<LPH>(dot_raw<T, W>(ow, vw));
           const float p = u < cnt ? ex2(s_ - m) : 0.f;
           const float pd = p * dp;
           l += pd;
