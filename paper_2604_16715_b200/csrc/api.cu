@@ -163,6 +163,8 @@ void gt_plan_s::mark_end(int stage, cudaStream_t st, cudaEvent_t a) {
 }
 
 gt_plan_s::~gt_plan_s() {
+  for (cudaEvent_t e : {ev_bwd0, ev_rows, ev_side})
+    if (e) cudaEventDestroy(e);
   for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
@@ -230,7 +232,8 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   const int64_t D = (int64_t)heads * d;
   const int elt = opts->dtype == GT_F32 ? 4 : 2;
   P->kv_row_bytes = 2 * D * elt;
-  P->in_row_bytes = round16(2 * D * elt + 8 * heads);
+  P->st_row_bytes = round16(8 * heads);
+  P->in_row_bytes = P->kv_row_bytes + P->st_row_bytes;
 
   gt_status cst = GT_OK;
   if (world > 1) {
@@ -310,7 +313,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       int64_t need = f.recv_rows * P->kv_row_bytes + b.recv_rows * P->in_row_bytes +
                      std::max((int64_t)f.send_idx.size() * P->kv_row_bytes, (int64_t)b.send_idx.size() * P->in_row_bytes) +
                      (c == GT_ALLGATHER ? P->n_max * (P->kv_row_bytes + P->in_row_bytes) : 0);
-      double fits = (double)need < 0.85 * (double)free_b ? 1.0 : 0.0;
+      double misfit = (double)need < 0.85 * (double)free_b ? 0.0 : 1.0;
+      GT_TRY(P->comm->max_host(&misfit, st));  // every rank must agree (the probe below is collective)
+      const double fits = misfit > 0 ? 0.0 : 1.0;
       double t_ex = INFINITY;
       if (strategy == GT_AUTO && fits > 0) {
         // measure the forward and backward exchanges of this pattern (2 warm-up + 3 timed)
@@ -390,11 +395,16 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     P->n_send_in = (int64_t)b.send_idx.size();
     GT_TRY(upload(P->d_send_out_idx, f.send_idx.data(), f.send_idx.size()));
     GT_TRY(upload(P->d_send_in_idx, b.send_idx.data(), b.send_idx.size()));
-    int64_t sbytes = std::max((int64_t)f.send_idx.size() * P->kv_row_bytes, (int64_t)b.send_idx.size() * P->in_row_bytes);
-    if (ag) sbytes = std::max(P->n_max * P->kv_row_bytes, P->n_max * P->in_row_bytes);
+    int64_t sbytes = std::max((int64_t)f.send_idx.size(), (int64_t)b.send_idx.size()) * P->kv_row_bytes;
+    if (ag) sbytes = P->n_max * P->kv_row_bytes;
     GT_TRY(P->d_send_buf.alloc((size_t)std::max<int64_t>(sbytes, 16)));
     GT_TRY(P->d_recv_kv.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
-    GT_TRY(P->d_recv_in.alloc((size_t)std::max<int64_t>(b.recv_rows * P->in_row_bytes, 16)));
+    GT_TRY(P->d_recv_qd.alloc((size_t)std::max<int64_t>(b.recv_rows * P->kv_row_bytes, 16)));
+    GT_TRY(P->d_recv_st.alloc((size_t)std::max<int64_t>(b.recv_rows * P->st_row_bytes, 16)));
+    GT_TRY(P->d_send_st.alloc((size_t)std::max<int64_t>((ag ? P->n_max : (int64_t)b.send_idx.size()) * P->st_row_bytes, 16)));
+    GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_bwd0, cudaEventDisableTiming));
+    GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_rows, cudaEventDisableTiming));
+    GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_side, cudaEventDisableTiming));
     int64_t recv_f = 0, recv_b = 0, send_f = 0, send_b = 0;
     for (int s = 0; s < world; ++s) {
       if (s == P->rank) continue;
@@ -448,7 +458,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
-                          &P->d_recv_kv, &P->d_recv_in})
+                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st})
     dev += (int64_t)b->bytes;
   I.device_bytes = dev;
   *out = P.release();
@@ -574,27 +584,47 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
   const void* halo_kv = P->world > 1 ? P->d_recv_kv.p : nullptr;
-  cudaEvent_t ev = nullptr;
+  cudaEvent_t ev = nullptr, ev2 = nullptr;
+  const bool multi = P->world > 1;
+  const bool ag = P->strategy == GT_ALLGATHER;
+  if (multi) {
+    // Side stream, overlapped with the row pass: [q | dy] rows of the in-halo are known at entry.
+    // Both messages go on the side stream so the communicator sees one ordered sequence.
+    const int elt = P->dtype == GT_F32 ? 4 : 2;
+    const int64_t D = (int64_t)P->heads * P->d;
+    GT_CUDA_TRY(cudaEventRecord(P->ev_bwd0, st));
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_bwd0, 0));
+    P->mark_begin(3, P->side, &ev2);
+    GT_TRY(pack_kv(q, dy, P->d_send_in_idx.as<int32_t>(), P->n_send_in, D, elt, P->d_send_buf.p, P->side));
+    if (ag)
+      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_qd.p, P->n_max, P->kv_row_bytes, P->side));
+    else
+      GT_TRY(P->comm->exchange(P->d_send_buf.p, P->si_off.data(), P->si_cnt.data(), P->d_recv_qd.p,
+                               P->ri_off.data(), P->ri_cnt.data(), P->kv_row_bytes, P->side));
+    P->mark_end(3, P->side, ev2);
+  }
   P->mark_begin(2, st, &ev);
   GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
   P->mark_end(2, st, ev);
-  const void* halo_in = nullptr;
-  if (P->world > 1) {
-    P->mark_begin(3, st, &ev);
-    const int elt = P->dtype == GT_F32 ? 4 : 2;
-    const int64_t D = (int64_t)P->heads * P->d;
-    GT_TRY(pack_in(q, dy, P->d_stats.as<float>(), P->d_send_in_idx.as<int32_t>(), P->n_send_in, D, P->heads, elt,
-                   P->d_send_buf.p, st));
-    if (P->strategy == GT_ALLGATHER)
-      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_in.p, P->n_max, P->in_row_bytes, st));
+  if (multi) {
+    // (LSE2, D) blocks of the in-halo rows: written by the row pass on their owners
+    GT_CUDA_TRY(cudaEventRecord(P->ev_rows, st));
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_rows, 0));
+    P->mark_begin(3, P->side, &ev2);
+    GT_TRY(pack_stats(P->d_stats.as<float>(), P->d_send_in_idx.as<int32_t>(), P->n_send_in, P->st_row_bytes,
+                      P->d_send_st.p, P->side));
+    if (ag)
+      GT_TRY(P->comm->all_gather(P->d_send_st.p, P->d_recv_st.p, P->n_max, P->st_row_bytes, P->side));
     else
-      GT_TRY(P->comm->exchange(P->d_send_buf.p, P->si_off.data(), P->si_cnt.data(), P->d_recv_in.p,
-                               P->ri_off.data(), P->ri_cnt.data(), P->in_row_bytes, st));
-    halo_in = P->d_recv_in.p;
-    P->mark_end(3, st, ev);
+      GT_TRY(P->comm->exchange(P->d_send_st.p, P->si_off.data(), P->si_cnt.data(), P->d_recv_st.p,
+                               P->ri_off.data(), P->ri_cnt.data(), P->st_row_bytes, P->side));
+    P->mark_end(3, P->side, ev2);
+    GT_CUDA_TRY(cudaEventRecord(P->ev_side, P->side));
+    GT_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_side, 0));
   }
   P->mark_begin(4, st, &ev);
-  GT_TRY(launch_bwd_cols(P, q, k, v, dy, halo_in, dk, dv, st));
+  GT_TRY(launch_bwd_cols(P, q, k, v, dy, multi ? P->d_recv_qd.p : nullptr, multi ? P->d_recv_st.p : nullptr, dk,
+                         dv, st));
   P->mark_end(4, st, ev);
   return GT_OK;
 }

@@ -117,7 +117,8 @@ struct PArgs {
   const char* ga;        // local tensor gathered first  (k | k | q)
   const char* gb;        // local tensor gathered second (v | v | dy)
   const char* gs;        // local (LSE2, D) rows [n_local][SB bytes] (pass 2)
-  const char* halo;      // packed remote rows
+  const char* halo;      // packed remote rows: [k | v] (passes 0, 1) or [q | dy] (pass 2)
+  const char* halo_s;    // pass 2: remote (LSE2, D) blocks [rows][SB bytes]
   int64_t halo_stride;
   int64_t n_local;
   const char* oa;        // own tensor A (q | q | k)
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
         const char* hrow = a.halo + (cv - a.n_local) * a.halo_stride;
         pa = loc ? a.ga + cv * RB : hrow;
         pb = loc ? a.gb + cv * RB : hrow + RB;
-        if constexpr (PASS == 2) ps = loc ? a.gs + cv * C::SB : hrow + 2 * RB;
+        if constexpr (PASS == 2) ps = loc ? a.gs + cv * C::SB : a.halo_s + (cv - a.n_local) * C::SB;
       } else {
         pa = a.ga + cv * RB;
         pb = a.gb + cv * RB;
@@ -630,7 +631,8 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
 
 // Runs one pass with the pipelined kernel (merges of chunked rows are launched by the caller).
 gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b, const float* lse,
-                    const void* gather_a, const void* gather_b, const void* halo, void* out_a, void* out_b,
+                    const void* gather_a, const void* gather_b, const void* halo, const void* halo_s,
+                    void* out_a, void* out_b,
                     float* out_f, cudaStream_t st) {
   pipe::PArgs a{};
   const bool rows = pass != 2;
@@ -644,7 +646,8 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b
   a.gb = (const char*)gather_b;
   a.gs = (const char*)P->d_stats.p;
   a.halo = (const char*)halo;
-  a.halo_stride = rows ? P->kv_row_bytes : P->in_row_bytes;
+  a.halo_s = (const char*)halo_s;
+  a.halo_stride = P->kv_row_bytes;  // [k | v] and [q | dy] rows have the same size
   a.n_local = P->n_local;
   a.oa = (const char*)own_a;
   a.ob = (const char*)own_b;

@@ -1,8 +1,9 @@
 // Exchange layer: pack kernels, NCCL transport (loaded at run time), in-process loopback transport.
 //
 // Forward exchange (Alg. 1 lines 2 and 5): K||V rows of remote columns, packed
-// [k | v] per row.  Backward exchange (reading Z11, transposed owner): Q||dY||(LSE2, D) rows of
-// in-neighbour rows, packed [q | dy | stats] per row, padded to 16 bytes.
+// [k | v] per row.  Backward exchange (reading Z11, transposed owner), in two messages so the first
+// overlaps the row pass: [q | dy] rows of in-neighbour rows (known at backward entry), then their
+// (LSE2, D) blocks (written by the row pass).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdint.h>
@@ -34,19 +35,12 @@ __global__ void pack_kv_kernel(const uint4* k, const uint4* v, const int32_t* id
   }
 }
 
-__global__ void pack_in_kernel(const uint4* q, const uint4* dy, const uint4* stats, const int32_t* idx,
-                               int64_t rows, int vec, int svec, int64_t row_vec, uint4* out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < rows; r += nw) {
-    const int64_t src = idx[r];
-    uint4* o = out + r * row_vec;
-    for (int c = lane; c < vec; c += 32) {
-      o[c] = q[src * vec + c];
-      o[vec + c] = dy[src * vec + c];
-    }
-    if (lane < svec) o[2 * vec + lane] = stats[src * svec + lane];  // (LSE2, D) block, 16-byte padded
+__global__ void pack_stats_kernel(const uint4* stats, const int32_t* idx, int64_t rows, int svec, uint4* out) {
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows * svec; t += nt) {
+    const int64_t r = t / svec;
+    const int c = (int)(t % svec);
+    out[r * svec + c] = stats[(int64_t)idx[r] * svec + c];
   }
 }
 
@@ -62,15 +56,12 @@ gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows
   return GT_OK;
 }
 
-gt_status pack_in(const void* q, const void* dy, const float* stats, const int32_t* idx, int64_t rows, int64_t D,
-                  int heads, int elt, void* out, cudaStream_t st) {
+gt_status pack_stats(const float* stats, const int32_t* idx, int64_t rows, int64_t row_bytes, void* out,
+                     cudaStream_t st) {
   if (rows <= 0) return GT_OK;
-  const int vec = (int)(D * elt / 16);
-  const int64_t row_bytes = (2 * D * elt + 8 * heads + 15) / 16 * 16;
-  int64_t blocks = std::min<int64_t>((rows + 7) / 8, 148 * 16);
-  const int svec = (8 * heads + 15) / 16;
-  pack_in_kernel<<<(int)blocks, 256, 0, st>>>((const uint4*)q, (const uint4*)dy, (const uint4*)stats, idx, rows,
-                                               vec, svec, row_bytes / 16, (uint4*)out);
+  const int svec = (int)(row_bytes / 16);
+  const int64_t blocks = std::min<int64_t>((rows * svec + 255) / 256, 148 * 8);
+  pack_stats_kernel<<<(int)blocks, 256, 0, st>>>((const uint4*)stats, idx, rows, svec, (uint4*)out);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
 }

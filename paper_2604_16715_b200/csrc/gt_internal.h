@@ -122,8 +122,12 @@ struct gt_plan_s {
   int64_t n_send_out = 0, n_send_in = 0;                  // rows packed per exchange
   int64_t halo_out_rows = 0, halo_in_rows = 0;            // rows of the receive tables
   gt::DevBuf d_send_out_idx, d_send_in_idx;               // int32 local ids to pack
-  gt::DevBuf d_send_buf, d_recv_kv, d_recv_in;            // packed rows
-  int64_t kv_row_bytes = 0, in_row_bytes = 0;
+  gt::DevBuf d_send_buf, d_recv_kv;                       // packed rows: forward [k | v], backward [q | dy]
+  gt::DevBuf d_recv_qd, d_send_st, d_recv_st;             // backward [q | dy] rows, (LSE2, D) blocks
+  int64_t kv_row_bytes = 0;                               // 2 D b: one [k | v] or [q | dy] row
+  int64_t st_row_bytes = 0;                               // round16(8 heads): one (LSE2, D) block
+  int64_t in_row_bytes = 0;                               // kv + st: bytes per backward-halo row
+  cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr;
   bool fwd_done = false;
 
   // end-to-end host staging
@@ -150,20 +154,20 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st);
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
-                          const void* halo_in, void* dk, void* dv, cudaStream_t st);
+                          const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st);
 bool shape_supported(int heads, int d, int dtype);
 int launches_fwd(const gt_plan_s* P);
 int launches_bwd(const gt_plan_s* P);
 
 gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b, const float* lse,
-                    const void* gather_a, const void* gather_b, const void* halo, void* out_a, void* out_b,
-                    float* out_f, cudaStream_t st);
+                    const void* gather_a, const void* gather_b, const void* halo, const void* halo_s,
+                    void* out_a, void* out_b, float* out_f, cudaStream_t st);
 
 // pack kernels (comm.cu)
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,
                   void* out, cudaStream_t st);
-gt_status pack_in(const void* q, const void* dy, const float* stats, const int32_t* idx, int64_t rows,
-                  int64_t D, int heads, int elt, void* out, cudaStream_t st);
+gt_status pack_stats(const float* stats, const int32_t* idx, int64_t rows, int64_t row_bytes, void* out,
+                     cudaStream_t st);
 
 // graph (graph.cu)
 gt_status build_csc_device(const int64_t* d_row_ptr, const int32_t* d_col, int64_t n, int64_t nnz,
