@@ -49,6 +49,14 @@ static gt_status upload(DevBuf& b, const V* src, size_t count) {
   return GT_OK;
 }
 
+static gt_status upload_work(WorkList& w) {
+  GT_TRY(upload(w.d_beg, w.beg.data(), w.beg.size()));
+  GT_TRY(upload(w.d_end, w.end.data(), w.end.size()));
+  GT_TRY(upload(w.d_own, w.own.data(), w.own.size()));
+  GT_TRY(w.d_counter.alloc(sizeof(unsigned long long)));
+  return GT_OK;
+}
+
 static gt_status upload_chunks(ChunkTable& t) {
   if (t.nchunks() == 0) return GT_OK;
   GT_TRY(upload(t.d_ids, t.ids.data(), t.ids.size()));
@@ -163,7 +171,7 @@ void gt_plan_s::mark_end(int stage, cudaStream_t st, cudaEvent_t a) {
 }
 
 gt_plan_s::~gt_plan_s() {
-  for (cudaEvent_t e : {ev_bwd0, ev_rows, ev_side})
+  for (cudaEvent_t e : {ev_bwd0, ev_rows, ev_side, ev_fwd0, ev_halo})
     if (e) cudaEventDestroy(e);
   for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
   for (auto e : ev_pool) cudaEventDestroy(e);
@@ -224,10 +232,6 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   P->scale = opts->scale > 0.f ? opts->scale : (float)(1.0 / std::sqrt((double)heads * d));
   P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 1024;
   P->profile = opts->profile != 0;
-  {
-    const char* kv = getenv("GT_KERNEL");
-    P->kernel = (kv && std::string(kv) == "v1") ? 1 : 2;
-  }
   P->stats_stride = (int)((8 * heads + 15) / 16 * 16 / 4);
   const int64_t D = (int64_t)heads * d;
   const int elt = opts->dtype == GT_F32 ? 4 : 2;
@@ -417,26 +421,45 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     P->info.send_bwd_bytes = send_b * P->in_row_bytes;
   }
 
-  // ---- degree binning: rows / columns split into chunks ----
-  build_chunks(rp_local.data(), P->n_local, P->heavy_threshold, &P->heavy_rows);
-  build_chunks(P->h_col_ptr.data(), P->n_local, P->heavy_threshold, &P->heavy_cols);
-  GT_TRY(upload_chunks(P->heavy_rows));
-  GT_TRY(upload_chunks(P->heavy_cols));
+  // ---- degree binning and work lists (rows / columns split into chunks) ----
   {
-    std::vector<int32_t> ir = build_items(rp_local.data(), P->n_local, P->heavy_threshold, P->heavy_rows);
-    std::vector<int32_t> ic = build_items(P->h_col_ptr.data(), P->n_local, P->heavy_threshold, P->heavy_cols);
-    P->n_items_rows = (int64_t)ir.size();
-    P->n_items_cols = (int64_t)ic.size();
-    GT_TRY(upload(P->d_items_rows, ir.data(), ir.size()));
-    GT_TRY(upload(P->d_items_cols, ic.data(), ic.size()));
-    std::vector<int64_t> pr = build_item_ptr(rp_local.data(), P->n_local, ir, P->heavy_rows);
-    std::vector<int64_t> pc = build_item_ptr(P->h_col_ptr.data(), P->n_local, ic, P->heavy_cols);
-    GT_TRY(upload(P->d_iptr_rows, pr.data(), pr.size()));
-    GT_TRY(upload(P->d_iptr_cols, pc.data(), pc.size()));
-    GT_TRY(P->d_counters.alloc(4 * sizeof(unsigned long long)));
+    const int64_t T = P->heavy_threshold;
+    build_work(P->n_local, [&](int64_t r, std::vector<Segment>& o) { o.push_back({rp_local[r], rp_local[r + 1], 0}); },
+               T, 1, &P->w_rows, &P->heavy_rows);
+    build_work(P->n_local,
+               [&](int64_t c, std::vector<Segment>& o) { o.push_back({P->h_col_ptr[c], P->h_col_ptr[c + 1], 0}); }, T,
+               1, &P->w_cols, &P->heavy_cols);
+    if (!single) {
+      // forward split: entries [e0, a) and [b, e1) of a row have remote columns (global column < lo or
+      // >= hi; columns are sorted), [a, b) owned columns
+      P->fwd_split = true;
+      const int64_t lo = P->lo, hi = P->hi;
+      build_work(P->n_local,
+                 [&](int64_t r, std::vector<Segment>& o) {
+                   const int64_t g0 = csr->row_ptr[lo + r], g1 = csr->row_ptr[lo + r + 1];
+                   const int32_t* c0 = csr->col_idx + g0;
+                   const int32_t* c1 = csr->col_idx + g1;
+                   const int64_t a = std::lower_bound(c0, c1, (int32_t)lo) - c0;
+                   const int64_t b = std::lower_bound(c0, c1, (int32_t)hi) - c0;
+                   const int64_t base = rp_local[r];
+                   o.push_back({base, base + a, 1});
+                   o.push_back({base + a, base + b, 0});
+                   o.push_back({base + b, base + (g1 - g0), 1});
+                 },
+                 T, 2, P->w_fwd, &P->fwd_chunks);
+      GT_TRY(upload_chunks(P->fwd_chunks));
+      for (auto* w : {&P->w_fwd[0], &P->w_fwd[1]}) GT_TRY(upload_work(*w));
+      GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fwd0, cudaEventDisableTiming));
+      GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_halo, cudaEventDisableTiming));
+    }
+    GT_TRY(upload_chunks(P->heavy_rows));
+    GT_TRY(upload_chunks(P->heavy_cols));
+    GT_TRY(upload_work(P->w_rows));
+    GT_TRY(upload_work(P->w_cols));
   }
   const int64_t nrc = P->heavy_rows.nchunks(), ncc = P->heavy_cols.nchunks();
-  GT_TRY(P->d_part_fwd.alloc((size_t)std::max<int64_t>(nrc, 1) * (D + 2 * heads) * sizeof(float)));
+  const int64_t nfc = P->fwd_split ? P->fwd_chunks.nchunks() : nrc;
+  GT_TRY(P->d_part_fwd.alloc((size_t)std::max<int64_t>(nfc, 1) * (D + 2 * heads) * sizeof(float)));
   GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * (2 * D + heads) * sizeof(float)));
   GT_TRY(P->d_part_colb.alloc((size_t)std::max<int64_t>(ncc, 1) * (2 * D) * sizeof(float)));
   GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->stats_stride * sizeof(float)));
@@ -556,22 +579,26 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
   const void* halo = nullptr;
-  cudaEvent_t ev = nullptr;
+  cudaEvent_t ev = nullptr, ev2 = nullptr;
   if (P->world > 1) {
+    // K||V rows of the halo on the side stream, overlapped with phase A (owned-column entries)
     const int elt = P->dtype == GT_F32 ? 4 : 2;
     const int64_t D = (int64_t)P->heads * P->d;
-    P->mark_begin(0, st, &ev);
-    GT_TRY(pack_kv(k, v, P->d_send_out_idx.as<int32_t>(), P->n_send_out, D, elt, P->d_send_buf.p, st));
+    GT_CUDA_TRY(cudaEventRecord(P->ev_fwd0, st));
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_fwd0, 0));
+    P->mark_begin(0, P->side, &ev2);
+    GT_TRY(pack_kv(k, v, P->d_send_out_idx.as<int32_t>(), P->n_send_out, D, elt, P->d_send_buf.p, P->side));
     if (P->strategy == GT_ALLGATHER)
-      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_kv.p, P->n_max, P->kv_row_bytes, st));
+      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_kv.p, P->n_max, P->kv_row_bytes, P->side));
     else
       GT_TRY(P->comm->exchange(P->d_send_buf.p, P->so_off.data(), P->so_cnt.data(), P->d_recv_kv.p,
-                               P->ro_off.data(), P->ro_cnt.data(), P->kv_row_bytes, st));
+                               P->ro_off.data(), P->ro_cnt.data(), P->kv_row_bytes, P->side));
+    P->mark_end(0, P->side, ev2);
+    GT_CUDA_TRY(cudaEventRecord(P->ev_halo, P->side));
     halo = P->d_recv_kv.p;
-    P->mark_end(0, st, ev);
   }
   P->mark_begin(1, st, &ev);
-  GT_TRY(launch_fwd(P, q, k, v, halo, y, lse, st));
+  GT_TRY(launch_fwd(P, q, k, v, halo, y, lse, st, P->world > 1 ? P->ev_halo : nullptr));
   P->mark_end(1, st, ev);
   P->fwd_done = true;
   return GT_OK;

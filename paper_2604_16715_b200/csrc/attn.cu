@@ -25,6 +25,7 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kBlock = 256;
+constexpr int kReserveSms = 16;   // SMs left to NCCL kernels while the forward halo is in flight
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -217,18 +218,32 @@ bool shape_supported(int heads, int d, int dtype) {
 }
 
 int launches_fwd(const gt_plan_s* P) {
-  return (P->n_items_rows > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
+  if (P->fwd_split)
+    return (P->w_fwd[0].n > 0 ? 1 : 0) + (P->w_fwd[1].n > 0 ? 1 : 0) + (P->fwd_chunks.nchunks() > 0 ? 1 : 0);
+  return (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
 }
 int launches_bwd(const gt_plan_s* P) {
-  return (P->n_items_rows > 0 ? 1 : 0) + (P->n_items_cols > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0) +
+  return (P->w_rows.n > 0 ? 1 : 0) + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0) +
          (P->heavy_cols.nchunks() > 0 ? 1 : 0);
 }
 
+// Forward.  world == 1: one pass over all rows.  world > 1: phase A (owned-column entries) runs while
+// the K||V halo is in flight on the side stream, leaving a few SMs to the communication kernels;
+// phase B (remote-column entries) waits for `halo_ready`; rows split across phases are merged.
 gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv, void* y,
-                     float* lse, cudaStream_t st) {
-  GT_TRY(pipe_pass(P, 0, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st));
-  if (P->heavy_rows.nchunks() > 0) {
-    MergeArgs m = merge_args(P->heavy_rows, P->d_part_fwd, P->scale);
+                     float* lse, cudaStream_t st, cudaEvent_t halo_ready) {
+  float* part = P->d_part_fwd.as<float>();
+  const ChunkTable& ct = P->fwd_split ? P->fwd_chunks : P->heavy_rows;
+  if (!P->fwd_split) {
+    GT_TRY(pipe_pass(P, 0, P->w_rows, ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0));
+  } else {
+    GT_TRY(pipe_pass(P, 0, P->w_fwd[0], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st,
+                     kReserveSms));
+    if (halo_ready) GT_CUDA_TRY(cudaStreamWaitEvent(st, halo_ready, 0));
+    GT_TRY(pipe_pass(P, 0, P->w_fwd[1], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0));
+  }
+  if (ct.nchunks() > 0) {
+    MergeArgs m = merge_args(ct, P->d_part_fwd, P->scale);
     m.y = (char*)y;
     m.lse = lse;
     GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 0, m, st));
@@ -238,7 +253,8 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
 
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st) {
-  GT_TRY(pipe_pass(P, 1, q, dy, lse, k, v, halo_kv, nullptr, dq, nullptr, P->d_stats.as<float>(), st));
+  GT_TRY(pipe_pass(P, 1, P->w_rows, P->heavy_rows, P->d_part_rowb.as<float>(), q, dy, lse, k, v, halo_kv, nullptr,
+                   dq, nullptr, P->d_stats.as<float>(), st, 0));
   if (P->heavy_rows.nchunks() > 0) {
     MergeArgs m = merge_args(P->heavy_rows, P->d_part_rowb, P->scale);
     m.dq = (char*)dq;
@@ -251,7 +267,8 @@ gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void
 
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
                           const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st) {
-  GT_TRY(pipe_pass(P, 2, k, v, nullptr, q, dy, halo_qd, halo_st, dk, dv, nullptr, st));
+  GT_TRY(pipe_pass(P, 2, P->w_cols, P->heavy_cols, P->d_part_colb.as<float>(), k, v, nullptr, q, dy, halo_qd,
+                   halo_st, dk, dv, nullptr, st, 0));
   if (P->heavy_cols.nchunks() > 0) {
     MergeArgs m = merge_args(P->heavy_cols, P->d_part_colb, P->scale);
     m.dk = (char*)dk;

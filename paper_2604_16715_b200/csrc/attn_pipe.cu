@@ -108,10 +108,12 @@ struct PC {
 };
 
 struct PArgs {
-  const int64_t* iptr;   // [nitems + 1] edge range of each item
+  const int64_t* ibeg;   // [nitems] entry range [ibeg, iend) of each item in the neighbour array
+  const int64_t* iend;
   const int32_t* iown;   // [nitems]: >= 0 row/column id, < 0 chunk -1 - c
   const int32_t* cown;   // chunk -> row/column id
-  const int32_t* nbr;    // neighbour ids in edge order (remapped: < n_local local, else halo slot)
+  const int32_t* nbr;    // neighbour ids in entry order (remapped: < n_local local, else halo slot)
+  int64_t nnbr;          // entries in nbr
   int64_t nitems;
   unsigned long long* counter;
   const char* ga;        // local tensor gathered first  (k | k | q)
@@ -303,14 +305,14 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
   char* const owns = stages + kS * C::STAGE;                 // kS * OWNP
 
   // ---------------- producer state (warp-uniform; per-lane only the tables) ----------------
-  int64_t t_next = 0, t_end = 0, batch_t0 = 0, batch_e1 = 0;
-  int64_t my_ptr = 0;                // lane k <= kG: iptr[batch_t0 + k]
-  int32_t my_own = 0;                // lane k < kG: iown[batch_t0 + k]
+  int64_t t_next = 0, t_end = 0, batch_t0 = 0;
+  int64_t my_beg = 0, my_end = 0;    // lane k < kG: entry range of item batch_t0 + k
+  int32_t my_own = 0;                // lane k < kG: owner of item batch_t0 + k
   bool done = false;
   int64_t pe = 0, pe_end = 0;        // current item's remaining edge range
   int32_t cur_own = 0;
   bool cur_first = false;
-  int64_t win_base = 0;              // lane l holds nbr[win_base + l] in win, nbr[win_base + 32 + l] in win_next
+  int64_t win_base = -(1ll << 40);   // lane l holds nbr[win_base + l] in win, nbr[win_base + 32 + l] in win_next
   int32_t win = 0, win_next = 0;
 
   auto finalize_empty = [&](int64_t r) {  // a row (column) with no entries
@@ -330,8 +332,8 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
 
   auto load_window = [&](int64_t base) {
     win_base = base;
-    win = (base + lane < batch_e1) ? __ldg(a.nbr + base + lane) : 0;
-    win_next = (base + 32 + lane < batch_e1) ? __ldg(a.nbr + base + 32 + lane) : 0;
+    win = (base + lane < a.nnbr) ? __ldg(a.nbr + base + lane) : 0;
+    win_next = (base + 32 + lane < a.nnbr) ? __ldg(a.nbr + base + 32 + lane) : 0;
   };
 
   // Advances to the next non-empty item; false when the grid's work is exhausted.
@@ -350,14 +352,14 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
         t_end = min(batch_t0 + kG, a.nitems);
         t_next = batch_t0;
         const int64_t k = batch_t0 + lane;
-        my_ptr = (lane <= kG && k <= a.nitems) ? __ldg(a.iptr + k) : 0;
-        my_own = (lane < kG && k < a.nitems) ? __ldg(a.iown + k) : 0;
-        batch_e1 = __shfl_sync(kFull, my_ptr, (int)(t_end - batch_t0));
-        load_window(__shfl_sync(kFull, my_ptr, 0));
+        const bool in = lane < kG && k < a.nitems;
+        my_beg = in ? __ldg(a.ibeg + k) : 0;
+        my_end = in ? __ldg(a.iend + k) : 0;
+        my_own = in ? __ldg(a.iown + k) : 0;
       }
       const int k = (int)(t_next - batch_t0);
-      const int64_t e0 = __shfl_sync(kFull, my_ptr, k);
-      const int64_t e1 = __shfl_sync(kFull, my_ptr, k + 1);
+      const int64_t e0 = __shfl_sync(kFull, my_beg, k);
+      const int64_t e1 = __shfl_sync(kFull, my_end, k);
       const int32_t own = __shfl_sync(kFull, my_own, k);
       ++t_next;
       if (e1 == e0) {
@@ -379,10 +381,12 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
     md.own = 0;
     md.first = md.last = false;
     if (pe >= pe_end && !next_item()) return md;
-    if (pe >= win_base + 32) {  // slide the neighbour window; prefetch the one after
+    if (pe == win_base + 32) {  // slide the neighbour window; prefetch the one after
       win_base += 32;
       win = win_next;
-      win_next = (win_base + 32 + lane < batch_e1) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
+      win_next = (win_base + 32 + lane < a.nnbr) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
+    } else if (pe < win_base || pe > win_base + 32) {
+      load_window(pe);  // items of a list need not be contiguous (split forward)
     }
     int64_t lim = pe_end - pe;
     if (win_base + 32 - pe < lim) lim = win_base + 32 - pe;
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
 
 // ----------------------------------------------------------------- launcher --
 template <typename T, int H, int D, int PASS, bool HALO>
-gt_status launch(const PArgs& a, cudaStream_t st) {
+gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
   using C = PC<T, H, D, PASS>;
   static int grid = 0;
   const size_t smem = (size_t)kWarps * C::WARP_SMEM;
@@ -592,7 +596,14 @@ gt_status launch(const PArgs& a, cudaStream_t st) {
   }
   if (a.nitems <= 0) return GT_OK;
   const int64_t want = (a.nitems + kG - 1) / kG;
-  const int g = (int)std::min<int64_t>(grid, (want + kWarps - 1) / kWarps);
+  int cap = grid;
+  if (reserve_sms > 0) {  // leave SMs free for concurrent communication kernels (overlap phases)
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = std::max(1, grid - grid / sms * reserve_sms);
+  }
+  const int g = (int)std::min<int64_t>(cap, (want + kWarps - 1) / kWarps);
   GT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
   pipe_kernel<T, H, D, PASS, HALO><<<g, kWarps * 32, smem, st>>>(a);
   GT_CUDA_TRY(cudaGetLastError());
@@ -601,21 +612,21 @@ gt_status launch(const PArgs& a, cudaStream_t st) {
 
 template <typename T, int H, int D>
 struct Ops {
-  static gt_status run(int pass, const PArgs& a, cudaStream_t st) {
+  static gt_status run(int pass, const PArgs& a, cudaStream_t st, int rs) {
     if (a.halo) {
-      if (pass == 0) return launch<T, H, D, 0, true>(a, st);
-      if (pass == 1) return launch<T, H, D, 1, true>(a, st);
-      return launch<T, H, D, 2, true>(a, st);
+      if (pass == 0) return launch<T, H, D, 0, true>(a, st, rs);
+      if (pass == 1) return launch<T, H, D, 1, true>(a, st, rs);
+      return launch<T, H, D, 2, true>(a, st, rs);
     }
-    if (pass == 0) return launch<T, H, D, 0, false>(a, st);
-    if (pass == 1) return launch<T, H, D, 1, false>(a, st);
-    return launch<T, H, D, 2, false>(a, st);
+    if (pass == 0) return launch<T, H, D, 0, false>(a, st, rs);
+    if (pass == 1) return launch<T, H, D, 1, false>(a, st, rs);
+    return launch<T, H, D, 2, false>(a, st, rs);
   }
 };
 
-gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream_t st) {
+gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream_t st, int rs) {
 #define GT_CASE(TT, HH, DD) \
-  if (H == HH && D == DD) return Ops<TT, HH, DD>::run(pass, a, st);
+  if (H == HH && D == DD) return Ops<TT, HH, DD>::run(pass, a, st, rs);
 #define GT_HCASES(TT)                                                                              \
   GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
   GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
@@ -629,19 +640,21 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
 
 }  // namespace pipe
 
-// Runs one pass with the pipelined kernel (merges of chunked rows are launched by the caller).
-gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b, const float* lse,
-                    const void* gather_a, const void* gather_b, const void* halo, const void* halo_s,
-                    void* out_a, void* out_b,
-                    float* out_f, cudaStream_t st) {
+// Runs one pass of the pipelined kernel over the work list `w` (chunks of `ct` write partial states
+// to `part`; their merges are launched by the caller).
+gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
+                    const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
+                    const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms) {
   pipe::PArgs a{};
   const bool rows = pass != 2;
-  a.iptr = (rows ? P->d_iptr_rows : P->d_iptr_cols).as<int64_t>();
-  a.iown = (rows ? P->d_items_rows : P->d_items_cols).as<int32_t>();
-  a.cown = (rows ? P->heavy_rows : P->heavy_cols).d_owner.as<int32_t>();
+  a.ibeg = w.d_beg.as<int64_t>();
+  a.iend = w.d_end.as<int64_t>();
+  a.iown = w.d_own.as<int32_t>();
+  a.nitems = w.n;
+  a.cown = ct.d_owner.as<int32_t>();
   a.nbr = (rows ? P->d_col : P->d_row).as<int32_t>();
-  a.nitems = rows ? P->n_items_rows : P->n_items_cols;
-  a.counter = P->d_counters.as<unsigned long long>() + pass;
+  a.nnbr = rows ? P->nnz_local : P->nnz_in_local;
+  a.counter = w.d_counter.as<unsigned long long>();
   a.ga = (const char*)gather_a;
   a.gb = (const char*)gather_b;
   a.gs = (const char*)P->d_stats.p;
@@ -655,10 +668,10 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b
   a.out_a = (char*)out_a;
   a.out_b = (char*)out_b;
   a.out_f = out_f;
-  a.part = (pass == 0 ? P->d_part_fwd : pass == 1 ? P->d_part_rowb : P->d_part_colb).as<float>();
+  a.part = part;
   a.qscale = P->scale * pipe::kLog2e;
   a.scale = P->scale;
-  return pipe::dispatch(P->dtype, P->heads, P->heads * P->d, pass, a, st);
+  return pipe::dispatch(P->dtype, P->heads, P->heads * P->d, pass, a, st, reserve_sms);
 }
 
 }  // namespace gt

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -77,6 +78,22 @@ struct ChunkTable {        // rows (or columns) split into chunks of <= chunk ed
   int64_t nchunks() const { return (int64_t)chunk_lo.size(); }
 };
 
+// Work items of one kernel launch: entry range [beg, end) in the CSR (CSC) slice and the owner
+// (>= 0: the row/column, finished in place; < 0: chunk -1 - c of a ChunkTable, merged later).
+// Listed in row (column) order so resident warps sweep a narrow window of rows.
+struct WorkList {
+  std::vector<int64_t> beg, end;
+  std::vector<int32_t> own;
+  DevBuf d_beg, d_end, d_own, d_counter;
+  int64_t n = 0;
+};
+
+// One segment of a row's entries assigned to a phase (0 or 1) of a split pass.
+struct Segment {
+  int64_t lo, hi;
+  int phase;
+};
+
 }  // namespace gt
 
 struct gt_plan_s {
@@ -96,18 +113,20 @@ struct gt_plan_s {
   gt::DevBuf d_row;                // int32[nnz_in_local]
   std::vector<int64_t> h_col_ptr;  // host copy of d_col_ptr (exports, chunking)
 
-  gt::ChunkTable heavy_rows, heavy_cols;
-  // work items in row (column) order: id >= 0 a whole row, id < 0 chunk (-1 - id) of a heavy row
-  gt::DevBuf d_items_rows, d_items_cols, d_counters;
-  gt::DevBuf d_iptr_rows, d_iptr_cols;     // int64[n_items + 1]: edge range of each item
-  int kernel = 2;                          // 2 = pipelined TMA kernels (attn_pipe.cu), 1 = v1 (attn.cu)
+  gt::ChunkTable heavy_rows, heavy_cols;   // rows / columns with more than heavy_threshold entries
+  gt::WorkList w_rows, w_cols;              // row pass (and unsplit forward), column pass
+  // forward with world > 1: phase A = owned-column entries (runs while K||V rows are exchanged),
+  // phase B = remote-column entries; rows touching both are chunks of fwd_chunks, merged at the end
+  bool fwd_split = false;
+  gt::WorkList w_fwd[2];
+  gt::ChunkTable fwd_chunks;
   int stats_stride = 0;                    // floats per row of d_stats: round16(8 heads) / 4
   int64_t n_items_rows = 0, n_items_cols = 0;
 
   // backward statistics: [n_local, heads, 2] fp32 = (LSE * log2(e), D)
   gt::DevBuf d_stats;
   // heavy-chunk workspaces (fp32)
-  gt::DevBuf d_part_fwd;           // [row chunks, D + 2 heads]
+  gt::DevBuf d_part_fwd;           // [forward chunks, D + 2 heads]
   gt::DevBuf d_part_rowb;          // [row chunks, 2 D + heads]
   gt::DevBuf d_part_colb;          // [col chunks, 2 D]
 
@@ -127,7 +146,7 @@ struct gt_plan_s {
   int64_t kv_row_bytes = 0;                               // 2 D b: one [k | v] or [q | dy] row
   int64_t st_row_bytes = 0;                               // round16(8 heads): one (LSE2, D) block
   int64_t in_row_bytes = 0;                               // kv + st: bytes per backward-halo row
-  cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr;
+  cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr, ev_fwd0 = nullptr, ev_halo = nullptr;
   bool fwd_done = false;
 
   // end-to-end host staging
@@ -150,7 +169,7 @@ struct gt_plan_s {
 namespace gt {
 // attention kernels (attn.cu)
 gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv, void* y,
-                     float* lse, cudaStream_t st);
+                     float* lse, cudaStream_t st, cudaEvent_t halo_ready);
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st);
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
@@ -159,9 +178,9 @@ bool shape_supported(int heads, int d, int dtype);
 int launches_fwd(const gt_plan_s* P);
 int launches_bwd(const gt_plan_s* P);
 
-gt_status pipe_pass(gt_plan_s* P, int pass, const void* own_a, const void* own_b, const float* lse,
-                    const void* gather_a, const void* gather_b, const void* halo, const void* halo_s,
-                    void* out_a, void* out_b, float* out_f, cudaStream_t st);
+gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
+                    const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
+                    const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms);
 
 // pack kernels (comm.cu)
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,
@@ -183,8 +202,10 @@ std::vector<int32_t> halo_set(int64_t n, const int64_t* row_ptr, const int32_t* 
 //   inward = 1 (backward): owned rows with an entry in a column of [blo, bhi) = H_peer^in n [lo, hi)
 std::vector<int32_t> send_set(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t lo, int64_t hi,
                               int64_t blo, int64_t bhi, bool inward);
-void build_chunks(const int64_t* ptr, int64_t count, int64_t threshold, ChunkTable* t);
-std::vector<int32_t> build_items(const int64_t* ptr, int64_t count, int64_t threshold, const ChunkTable& t);
-std::vector<int64_t> build_item_ptr(const int64_t* ptr, int64_t count, const std::vector<int32_t>& items,
-                                    const ChunkTable& t);
+// Builds the work lists of a pass: segs(r, out) lists row r's entry segments in entry order; a
+// segment longer than `threshold` is cut into equal chunks; a row with exactly one piece becomes a
+// whole-row item, otherwise every piece is a chunk of `t` (merged in entry order).  Rows without
+// entries become empty items in phase 0 (their outputs are written as empty rows).
+void build_work(int64_t count, const std::function<void(int64_t, std::vector<Segment>&)>& segs, int64_t threshold,
+                int nphase, WorkList* phases, ChunkTable* t);
 }  // namespace gt

@@ -135,45 +135,43 @@ std::vector<int32_t> send_set(int64_t n, const int64_t* rp, const int32_t* ci, i
   return out;
 }
 
-void build_chunks(const int64_t* ptr, int64_t count, int64_t threshold, ChunkTable* t) {
+void build_work(int64_t count, const std::function<void(int64_t, std::vector<Segment>&)>& segs, int64_t threshold,
+                int nphase, WorkList* phases, ChunkTable* t) {
   t->ids.clear(); t->first.clear(); t->chunk_lo.clear(); t->chunk_hi.clear(); t->chunk_owner.clear();
-  for (int64_t i = 0; i < count; ++i) {
-    int64_t a = ptr[i], b = ptr[i + 1];
-    if (b - a <= threshold) continue;
-    t->ids.push_back((int32_t)i);
-    t->first.push_back((int32_t)t->chunk_lo.size());
-    int64_t nch = (b - a + threshold - 1) / threshold;
-    // equal-size chunks (the last differs by at most one entry)
-    for (int64_t c = 0; c < nch; ++c) {
-      t->chunk_lo.push_back(a + (b - a) * c / nch);
-      t->chunk_hi.push_back(a + (b - a) * (c + 1) / nch);
-      t->chunk_owner.push_back((int32_t)i);
+  for (int ph = 0; ph < nphase; ++ph) {
+    phases[ph].beg.clear(); phases[ph].end.clear(); phases[ph].own.clear();
+  }
+  std::vector<Segment> sg, pieces;
+  for (int64_t r = 0; r < count; ++r) {
+    sg.clear();
+    segs(r, sg);
+    pieces.clear();
+    for (const Segment& s : sg) {
+      const int64_t len = s.hi - s.lo;
+      if (len <= 0) continue;
+      const int64_t nch = (len + threshold - 1) / threshold;  // equal chunks of <= threshold entries
+      for (int64_t c = 0; c < nch; ++c)
+        pieces.push_back({s.lo + len * c / nch, s.lo + len * (c + 1) / nch, s.phase});
+    }
+    if (pieces.empty()) {
+      const int64_t at = sg.empty() ? 0 : sg.front().lo;
+      phases[0].beg.push_back(at); phases[0].end.push_back(at); phases[0].own.push_back((int32_t)r);
+    } else if (pieces.size() == 1) {
+      WorkList& w = phases[pieces[0].phase];
+      w.beg.push_back(pieces[0].lo); w.end.push_back(pieces[0].hi); w.own.push_back((int32_t)r);
+    } else {
+      t->ids.push_back((int32_t)r);
+      t->first.push_back((int32_t)t->chunk_lo.size());
+      for (const Segment& p : pieces) {
+        const int32_t c = (int32_t)t->chunk_lo.size();
+        t->chunk_lo.push_back(p.lo); t->chunk_hi.push_back(p.hi); t->chunk_owner.push_back((int32_t)r);
+        WorkList& w = phases[p.phase];
+        w.beg.push_back(p.lo); w.end.push_back(p.hi); w.own.push_back(-1 - c);
+      }
     }
   }
   t->first.push_back((int32_t)t->chunk_lo.size());
-}
-
-std::vector<int32_t> build_items(const int64_t* ptr, int64_t count, int64_t threshold, const ChunkTable& t) {
-  std::vector<int32_t> items;
-  items.reserve((size_t)count + t.chunk_lo.size());
-  size_t h = 0;
-  for (int64_t i = 0; i < count; ++i) {
-    if (ptr[i + 1] - ptr[i] <= threshold) {
-      items.push_back((int32_t)i);
-      continue;
-    }
-    for (int32_t c = t.first[h]; c < t.first[h + 1]; ++c) items.push_back(-1 - c);
-    ++h;
-  }
-  return items;
-}
-
-std::vector<int64_t> build_item_ptr(const int64_t* ptr, int64_t count, const std::vector<int32_t>& items,
-                                    const ChunkTable& t) {
-  std::vector<int64_t> ip(items.size() + 1);
-  for (size_t k = 0; k < items.size(); ++k) ip[k] = items[k] >= 0 ? ptr[items[k]] : t.chunk_lo[-1 - items[k]];
-  ip[items.size()] = ptr[count];
-  return ip;
+  for (int ph = 0; ph < nphase; ++ph) phases[ph].n = (int64_t)phases[ph].beg.size();
 }
 
 }  // namespace gt
