@@ -321,10 +321,9 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
     for (int i = 0; i < EPL; ++i) z[i] = 0.f;
     stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, z);
     if constexpr (PASS == 0) {
-      if (lane % LPH == 0) a.out_f[r * H + head] = -INFINITY;
+      a.out_f[r * H + head] = -INFINITY;
     } else if constexpr (PASS == 1) {
-      if (lane % LPH == 0)
-        reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(-INFINITY, 0.f);
+      reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(-INFINITY, 0.f);
     } else {
       stg_f32<T, EPL>(a.out_b + r * RB + lane * LB, z);
     }
@@ -370,11 +369,12 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
       pe_end = e1;
       cur_own = own;
       cur_first = true;
-      // items of a list need not be contiguous (split forward; new batch): reload the window.
-      // (Pass 2 reloads unconditionally: with the data-dependent test ptxas can no longer prove
-      // the warp converged and emulates its shuffles - measured 1.4 ms slower on C3.)
-      if constexpr (PASS == 2) load_window(pe);
-      else if (pe < win_base || pe > win_base + 32) load_window(pe);
+      // items of a list need not be contiguous (split forward; new batch): reload the window.  Done
+      // unconditionally: with a data-dependent test (or lane-conditional stores, see below) ptxas can
+      // no longer prove the warp converged and emulates every shuffle (WARPSYNC.COLLECTIVE) - measured
+      // 3-8 % slower per pass on C3.  Per-head values are therefore stored by all lanes of the head
+      // (identical bytes, one sector) instead of under `if (lane % LPH == 0)`.
+      load_window(pe);
       return true;
     }
   };
@@ -543,12 +543,12 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
             float* pp = a.part + ch * (int64_t)(D + 2 * H);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
-            if (lane % LPH == 0) { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
+            { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
           } else if constexpr (PASS == 1) {
             float* pp = a.part + ch * (int64_t)(2 * D + H);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
-            if (lane % LPH == 0) pp[2 * D + head] = l;
+            pp[2 * D + head] = l;
           } else {
             float* pp = a.part + ch * (int64_t)(2 * D);
 #pragma unroll
@@ -561,13 +561,12 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] *= inv;
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
-            if (lane % LPH == 0) a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
+            a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
           } else if constexpr (PASS == 1) {
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] = a.scale * fmaf(-l, acc2[i], acc[i]);
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
-            if (lane % LPH == 0)
-              reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(m, l);
+            reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(m, l);
           } else {
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] *= a.scale;
