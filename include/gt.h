@@ -101,6 +101,12 @@ typedef struct {
   int heavy_threshold;     /* rows/columns with more entries are split into chunks; 0 => 1024 */
   const char* beta_profile;/* optional path of a measured-beta JSON; NULL => probe at plan time */
   int profile;             /* 1 => record CUDA events around every stage (gt_plan_timings) */
+  int edge_state;          /* per-entry state of the backward (Table 1 keeps U per edge,
+                              P:166): 0 => materialise when it fits in 85 % of free device memory,
+                              1 => materialise (GT_ENOMEM if it does not fit), -1 => never
+                              (recompute q.k and dY.v in the column pass).  Materialised, the row
+                              pass stores (P, dP) in fp32, 8 h B per owned-row entry, and the plan
+                              holds a 4 B CSC -> CSR map per owned-column entry. */
 } gt_opts;
 
 typedef struct {
@@ -123,6 +129,8 @@ typedef struct {
   double agp_score[4];            /* Alg. 3 score p * t_comm / (p - 1) per strategy (ms) */
   int agp_feasible[4];            /* Eq. 14 feasibility: score <= t_iter(1) */
   double alpha_s_per_unit;        /* cost-model compute seconds per (edge + row) */
+  int edge_state;                 /* 1 if the plan materialises per-entry state (gt_opts.edge_state) */
+  int64_t edge_state_bytes;       /* device bytes of that state */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,

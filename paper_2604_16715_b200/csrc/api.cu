@@ -265,8 +265,10 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   DevBuf* rw = single ? &P->d_row : &full_row;
   GT_TRY(cp->alloc(((size_t)n + 1) * sizeof(int64_t)));
   GT_TRY(rw->alloc(std::max<size_t>((size_t)nnz, 1) * sizeof(int32_t)));
+  DevBuf full_src;  // CSR entry of each CSC position (for the entry-state permutation)
+  GT_TRY(full_src.alloc(std::max<size_t>((size_t)nnz, 1) * sizeof(int32_t)));
   GT_TRY(build_csc_device(full_rp.as<int64_t>(), full_col->as<int32_t>(), n, nnz, cp->as<int64_t>(),
-                          rw->as<int32_t>(), st));
+                          rw->as<int32_t>(), full_src.as<int32_t>(), st));
   std::vector<int64_t> col_ptr_full((size_t)n + 1);
   GT_CUDA_TRY(cudaMemcpy(col_ptr_full.data(), cp->p, ((size_t)n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
 
@@ -452,12 +454,55 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fwd0, cudaEventDisableTiming));
       GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_halo, cudaEventDisableTiming));
     }
+    // ---- materialised entry state (opts.edge_state) ----
+    if (opts->edge_state < -1 || opts->edge_state > 1) return fail(GT_EINVAL, "gt_plan: edge_state must be -1, 0 or 1");
+    if (opts->edge_state >= 0) {
+      const int64_t es_bytes = P->nnz_local * heads * 8 + P->nnz_in_local * 4;
+      size_t free_b = 0, total_b = 0;
+      GT_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+      double misfit = (double)es_bytes < 0.85 * (double)free_b ? 0.0 : 1.0;
+      if (!single) GT_TRY(P->comm->max_host(&misfit, st));  // the column-pass split must agree across ranks
+      if (misfit > 0 && opts->edge_state == 1) return fail(GT_ENOMEM, "gt_plan: entry state does not fit in device memory");
+      P->es = misfit == 0;
+      P->info.edge_state_bytes = P->es ? es_bytes : 0;
+    }
+    if (P->es) {
+      GT_TRY(P->d_pd.alloc(((size_t)P->nnz_local * heads * 2 + 32) * sizeof(float)));  // + masked-store scratch
+      GT_TRY(P->d_src.alloc(std::max<size_t>((size_t)P->nnz_in_local, 1) * sizeof(int32_t)));
+      GT_TRY(build_local_src(full_src.as<int32_t>(), c0, c1, csr->row_ptr[P->lo], csr->row_ptr[P->hi],
+                             P->d_src.as<int32_t>(), st));
+      if (!single) {
+        // column split: CSC rows ascend within a column, so entries [e0, a) and [b, e1) have remote
+        // rows (global row < lo or >= hi), [a, b) owned rows
+        P->col_split = true;
+        std::vector<int32_t> grow((size_t)P->nnz_in_local);
+        if (P->nnz_in_local)
+          GT_CUDA_TRY(cudaMemcpy(grow.data(), full_row.as<int32_t>() + c0, grow.size() * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost));
+        const int64_t lo = P->lo, hi = P->hi;
+        build_work(P->n_local,
+                   [&](int64_t c, std::vector<Segment>& o) {
+                     const int64_t e0 = P->h_col_ptr[c], e1 = P->h_col_ptr[c + 1];
+                     const int32_t* r0 = grow.data() + e0;
+                     const int32_t* r1 = grow.data() + e1;
+                     const int64_t a = std::lower_bound(r0, r1, (int32_t)lo) - r0;
+                     const int64_t b = std::lower_bound(r0, r1, (int32_t)hi) - r0;
+                     o.push_back({e0, e0 + a, 1});
+                     o.push_back({e0 + a, e0 + b, 0});
+                     o.push_back({e0 + b, e1, 1});
+                   },
+                   T, 2, P->w_colp, &P->col_chunks);
+        GT_TRY(upload_chunks(P->col_chunks));
+        for (auto* w : {&P->w_colp[0], &P->w_colp[1]}) GT_TRY(upload_work(*w));
+      }
+    }
+    P->info.edge_state = P->es ? 1 : 0;
     GT_TRY(upload_chunks(P->heavy_rows));
     GT_TRY(upload_chunks(P->heavy_cols));
     GT_TRY(upload_work(P->w_rows));
     GT_TRY(upload_work(P->w_cols));
   }
-  const int64_t nrc = P->heavy_rows.nchunks(), ncc = P->heavy_cols.nchunks();
+  const int64_t nrc = P->heavy_rows.nchunks(), ncc = P->col_split ? P->col_chunks.nchunks() : P->heavy_cols.nchunks();
   const int64_t nfc = P->fwd_split ? P->fwd_chunks.nchunks() : nrc;
   GT_TRY(P->d_part_fwd.alloc((size_t)std::max<int64_t>(nfc, 1) * (D + 2 * heads) * sizeof(float)));
   GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * (2 * D + heads) * sizeof(float)));
@@ -481,7 +526,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
-                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st})
+                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_pd, &P->d_src})
     dev += (int64_t)b->bytes;
   I.device_bytes = dev;
   *out = P.release();
@@ -647,11 +692,11 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
                                P->ri_off.data(), P->ri_cnt.data(), P->st_row_bytes, P->side));
     P->mark_end(3, P->side, ev2);
     GT_CUDA_TRY(cudaEventRecord(P->ev_side, P->side));
-    GT_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_side, 0));
+    if (!P->col_split) GT_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_side, 0));
   }
   P->mark_begin(4, st, &ev);
   GT_TRY(launch_bwd_cols(P, q, k, v, dy, multi ? P->d_recv_qd.p : nullptr, multi ? P->d_recv_st.p : nullptr, dk,
-                         dv, st));
+                         dv, st, multi ? P->ev_side : nullptr));
   P->mark_end(4, st, ev);
   return GT_OK;
 }

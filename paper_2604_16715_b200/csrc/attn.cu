@@ -223,8 +223,24 @@ int launches_fwd(const gt_plan_s* P) {
   return (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
 }
 int launches_bwd(const gt_plan_s* P) {
-  return (P->w_rows.n > 0 ? 1 : 0) + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0) +
-         (P->heavy_cols.nchunks() > 0 ? 1 : 0);
+  const int rows = (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
+  if (P->col_split)
+    return rows + (P->w_colp[0].n > 0 ? 1 : 0) + (P->w_colp[1].n > 0 ? 1 : 0) + (P->col_chunks.nchunks() > 0 ? 1 : 0);
+  return rows + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_cols.nchunks() > 0 ? 1 : 0);
+}
+
+// Entry-state arguments of a pass (Table 1 keeps U per edge): the row pass stores
+// (P, dP) per entry in local CSR order; the column pass reads them through the CSC -> CSR map.
+static EntryState entry_state(gt_plan_s* P, int pass) {
+  EntryState e;
+  if (!P->es) return e;
+  if (pass == 1) {
+    e.out = P->d_pd.as<float>();
+  } else if (pass == 2) {
+    e.in = P->d_pd.as<float>();
+    e.src = P->d_src.as<int32_t>();
+  }
+  return e;
 }
 
 // Forward.  world == 1: one pass over all rows.  world > 1: phase A (owned-column entries) runs while
@@ -254,7 +270,7 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st) {
   GT_TRY(pipe_pass(P, 1, P->w_rows, P->heavy_rows, P->d_part_rowb.as<float>(), q, dy, lse, k, v, halo_kv, nullptr,
-                   dq, nullptr, P->d_stats.as<float>(), st, 0));
+                   dq, nullptr, P->d_stats.as<float>(), st, 0, entry_state(P, 1)));
   if (P->heavy_rows.nchunks() > 0) {
     MergeArgs m = merge_args(P->heavy_rows, P->d_part_rowb, P->scale);
     m.dq = (char*)dq;
@@ -265,12 +281,26 @@ gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void
   return GT_OK;
 }
 
+// Column pass.  With entry state and world > 1 the owned-row entries (phase A, stored (P, dP)) run
+// before `side_ready` (the in-halo [q | dy] rows and stats) is waited on; the remote-row entries
+// (phase B) recompute p and dP; columns split across the phases are merged.
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
-                          const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st) {
-  GT_TRY(pipe_pass(P, 2, P->w_cols, P->heavy_cols, P->d_part_colb.as<float>(), k, v, nullptr, q, dy, halo_qd,
-                   halo_st, dk, dv, nullptr, st, 0));
-  if (P->heavy_cols.nchunks() > 0) {
-    MergeArgs m = merge_args(P->heavy_cols, P->d_part_colb, P->scale);
+                          const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st,
+                          cudaEvent_t side_ready) {
+  const ChunkTable& ct = P->col_split ? P->col_chunks : P->heavy_cols;
+  float* part = P->d_part_colb.as<float>();
+  if (!P->col_split) {
+    if (side_ready) GT_CUDA_TRY(cudaStreamWaitEvent(st, side_ready, 0));
+    GT_TRY(pipe_pass(P, 2, P->w_cols, ct, part, k, v, nullptr, q, dy, halo_qd, halo_st, dk, dv, nullptr, st, 0,
+                     entry_state(P, 2)));
+  } else {
+    GT_TRY(pipe_pass(P, 2, P->w_colp[0], ct, part, k, v, nullptr, q, dy, nullptr, nullptr, dk, dv, nullptr, st, 0,
+                     entry_state(P, 2)));
+    if (side_ready) GT_CUDA_TRY(cudaStreamWaitEvent(st, side_ready, 0));
+    GT_TRY(pipe_pass(P, 2, P->w_colp[1], ct, part, k, v, nullptr, q, dy, halo_qd, halo_st, dk, dv, nullptr, st, 0));
+  }
+  if (ct.nchunks() > 0) {
+    MergeArgs m = merge_args(ct, P->d_part_colb, P->scale);
     m.dk = (char*)dk;
     m.dv = (char*)dv;
     GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 2, m, st));

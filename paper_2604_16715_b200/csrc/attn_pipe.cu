@@ -91,7 +91,7 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
   return d;
 }
 
-template <typename T, int H, int D, int PASS>
+template <typename T, int H, int D, int PASS, bool ES>
 struct PC {
   static constexpr int RB = D * (int)sizeof(T);          // bytes of one feature row
   static constexpr int EPL = D / 32;                      // elements per lane
@@ -99,12 +99,20 @@ struct PC {
   static constexpr int LPH = 32 / H;                      // lanes per head
   static constexpr int SB = (8 * H + 15) / 16 * 16;       // (LSE2, D) row of the stats array, padded
   static constexpr int EB = 2 * RB + (PASS == 2 ? SB : 0);                          // bytes per neighbour
-  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? 2 * RB + 4 * H : 2 * RB);
+  // own slot: fwd q | rowb q dY lse | colb [k v]   (ES: the column pass reads the (P, dP) the row
+  // pass stored and needs no own-column data)
+  static constexpr int OWN_DY = PASS == 1 ? RB : 0;
+  static constexpr int OWN_LSE = OWN_DY + RB;
+  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * H : (ES ? 0 : 2 * RB));
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
-  static constexpr int STAGE = (U * EB + 15) / 16 * 16;
+  // per-stage entry state (ES column pass): (P, dP)[U][H] f32x2 gathered from the row pass's store
+  static constexpr int AUX = (ES && PASS == 2) ? U * H * 8 : 0;
+  static constexpr int STAGE = (U * EB + AUX + 15) / 16 * 16;
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
-  static constexpr int WARP_SMEM = kS * (STAGE + OWNP);
+  static constexpr int XS = (ES && PASS == 1) ? U * H * 8 : 0;       // rowb ES: (P, dP) transpose scratch
+  static constexpr int WARP_SMEM = kS * (STAGE + OWNP + XS);
   static_assert(LB == 8 || LB % 16 == 0, "lane slice must be 8 bytes or a multiple of 16");
+  static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
 };
 
 struct PArgs {
@@ -131,6 +139,11 @@ struct PArgs {
   float* out_f;          // lse (pass 0) | stats [n_local][SB/4] (pass 1)
   float* part;           // chunk partials
   float qscale, scale;
+  // materialised entry state (ES kernels; Table 1 keeps U per edge)
+  float* es_out;         // rowb: (P, dP) [nnz_local][H][2] in local CSR entry order (+ 32 scratch floats)
+  int64_t es_scratch;    // rowb: float offset of the scratch slots (masked stores)
+  const float* es_in;    // colb: the same array
+  const int32_t* src;    // colb: local CSC position -> local CSR entry (read through a window like nbr)
 };
 
 // lane slice copy of one row: LB bytes at byte offset lane * LB
@@ -144,14 +157,21 @@ __device__ __forceinline__ void cp_slice(char* dst_row, const char* src_row, int
   }
 }
 
+// base + idx * stride with one mad.wide.u32 (64-bit result)
+__device__ __forceinline__ const char* row_addr(const char* base, uint32_t idx, uint32_t stride) {
+  const char* r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(idx), "r"(stride), "l"(base));
+  return r;
+}
+
+// this lane's LB bytes: dst and src already point at the lane's slice
 template <int LB>
-__device__ __forceinline__ void cp_slice_z(char* dst_row, const char* src_row, int lane, bool valid) {
+__device__ __forceinline__ void cp_lane_z(char* dst, const char* src, bool valid) {
   if constexpr (LB == 8) {
-    cp_async8z(dst_row + lane * 8, src_row + lane * 8, valid);
+    cp_async8z(dst, src, valid);
   } else {
 #pragma unroll
-    for (int i = 0; i < LB / 16; ++i)
-      cp_async16z(dst_row + lane * LB + 16 * i, src_row + lane * LB + 16 * i, valid);
+    for (int i = 0; i < LB / 16; ++i) cp_async16z(dst + 16 * i, src + 16 * i, valid);
   }
 }
 
@@ -287,15 +307,22 @@ __device__ __forceinline__ float head_sum(float x) {
 }
 
 struct Meta {      // warp-uniform description of one filled stage
+  int64_t e0;      // entry index (in `nbr` order) of the stage's first neighbour
   int32_t own;     // row/column id, or chunk -1 - c
   int32_t cnt;     // neighbours in the stage (0 = no work left)
   bool first, last;
 };
 
 // ------------------------------------------------------------------ kernel --
-template <typename T, int H, int D, int PASS, bool HALO>
-__global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
-  using C = PC<T, H, D, PASS>;
+// The ES row pass carries the stage entry offsets and the store pointer: hold it to 5 CTAs per SM
+// (<= 96 registers) where the lane slice is small enough not to spill.
+template <int PASS, bool ES, int EPL>
+constexpr int min_ctas() { return 1; }
+
+template <typename T, int H, int D, int PASS, bool HALO, bool ES>
+__global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) pipe_kernel(PArgs a) {
+  static_assert(!(ES && PASS == 2 && HALO), "the ES column pass reads local rows only");
+  using C = PC<T, H, D, PASS, ES>;
   constexpr int EPL = C::EPL, LPH = C::LPH, RB = C::RB, EB = C::EB, U = C::U, LB = C::LB;
   extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x & 31;
@@ -303,6 +330,7 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
   const int head = lane / LPH;
   char* const stages = smem + (size_t)wid * C::WARP_SMEM;   // kS * STAGE
   char* const owns = stages + kS * C::STAGE;                 // kS * OWNP
+  char* const xs = owns + kS * C::OWNP;                      // kS * XS
 
   // ---------------- producer state (warp-uniform; per-lane only the tables) ----------------
   int64_t t_next = 0, t_end = 0, batch_t0 = 0;
@@ -314,6 +342,14 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
   bool cur_first = false;
   int64_t win_base = -(1ll << 40);   // lane l holds nbr[win_base + l] in win, nbr[win_base + 32 + l] in win_next
   int32_t win = 0, win_next = 0;
+  int32_t wsrc = 0, wsrc_next = 0;   // ES column pass: src[] over the same window
+  // this lane's slice of row 0 of every gathered table: a row address is one mad.wide.u32
+  const char* const ga_l = a.ga + lane * LB;
+  const char* const gb_l = a.gb + lane * LB;
+  const char* const h_l = HALO ? a.halo + lane * LB : nullptr;
+  const char* const gs_l = PASS == 2 ? a.gs + lane * 16 : nullptr;
+  const char* const hs_l = (PASS == 2 && HALO) ? a.halo_s + lane * 16 : nullptr;
+  const uint32_t n_loc = (uint32_t)a.n_local;
 
   auto finalize_empty = [&](int64_t r) {  // a row (column) with no entries
     float z[EPL];
@@ -333,6 +369,10 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
     win_base = base;
     win = (base + lane < a.nnbr) ? __ldg(a.nbr + base + lane) : 0;
     win_next = (base + 32 + lane < a.nnbr) ? __ldg(a.nbr + base + 32 + lane) : 0;
+    if constexpr (ES && PASS == 2) {
+      wsrc = (base + lane < a.nnbr) ? __ldg(a.src + base + lane) : 0;
+      wsrc_next = (base + 32 + lane < a.nnbr) ? __ldg(a.src + base + 32 + lane) : 0;
+    }
   };
 
   // Advances to the next non-empty item; false when the grid's work is exhausted.
@@ -382,6 +422,7 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
   // Fills stage `s` with the next group of neighbours (this lane's slices) and returns its meta.
   auto produce = [&](int s) -> Meta {
     Meta md;
+    md.e0 = 0;
     md.cnt = 0;
     md.own = 0;
     md.first = md.last = false;
@@ -390,38 +431,48 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
       win_base += 32;
       win = win_next;
       win_next = (win_base + 32 + lane < a.nnbr) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
+      if constexpr (ES && PASS == 2) {
+        wsrc = wsrc_next;
+        wsrc_next = (win_base + 32 + lane < a.nnbr) ? __ldg(a.src + win_base + 32 + lane) : 0;
+      }
     }
-    int64_t lim = pe_end - pe;
-    if (win_base + 32 - pe < lim) lim = win_base + 32 - pe;
-    const int cnt = lim < U ? (int)lim : U;
-    char* st = stages + s * C::STAGE;
     const int off = (int)(pe - win_base);
+    const int cnt = min(min((int)(pe_end - pe), 32 - off), U);
+    char* st = stages + s * C::STAGE;
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // branch-free: neighbours u >= cnt are zero-filled, not read
       const bool valid = u < cnt;
-      const int64_t ci = __shfl_sync(kFull, win, (off + u) & 31);
-      const int64_t cv = valid ? ci : 0;
+      // shfl.idx reads the low 5 bits of the lane index; masked neighbours fetch some valid id
+      const uint32_t cv = (uint32_t)__shfl_sync(kFull, win, off + u);
       const char *pa, *pb, *ps = nullptr;
       if constexpr (HALO) {
-        const bool loc = cv < a.n_local;
-        const char* hrow = a.halo + (cv - a.n_local) * a.halo_stride;
-        pa = loc ? a.ga + cv * RB : hrow;
-        pb = loc ? a.gb + cv * RB : hrow + RB;
-        if constexpr (PASS == 2) ps = loc ? a.gs + cv * C::SB : a.halo_s + (cv - a.n_local) * C::SB;
+        const bool loc = cv < n_loc;
+        const char* hrow = row_addr(h_l, cv - n_loc, 2 * RB);
+        pa = loc ? row_addr(ga_l, cv, RB) : hrow;
+        pb = loc ? row_addr(gb_l, cv, RB) : hrow + RB;
+        if constexpr (PASS == 2) ps = loc ? row_addr(gs_l, cv, C::SB) : row_addr(hs_l, cv - n_loc, C::SB);
       } else {
-        pa = a.ga + cv * RB;
-        pb = a.gb + cv * RB;
-        if constexpr (PASS == 2) ps = a.gs + cv * C::SB;
+        pa = row_addr(ga_l, cv, RB);
+        pb = row_addr(gb_l, cv, RB);
+        if constexpr (PASS == 2) ps = row_addr(gs_l, cv, C::SB);
       }
-      char* dst = st + u * EB;
-      cp_slice_z<LB>(dst, pa, lane, valid);
-      cp_slice_z<LB>(dst + RB, pb, lane, valid);
+      char* dst = st + u * EB + lane * LB;
+      cp_lane_z<LB>(dst, pa, valid);
+      cp_lane_z<LB>(dst + RB, pb, valid);
       // (LSE2, D) block of the neighbour: SB / 16 lanes copy 16 bytes each (read by all lanes of a head
       // after the stage's wait + __syncwarp)
       if constexpr (PASS == 2) {
-        if (lane < C::SB / 16) cp_async16z(dst + 2 * RB + lane * 16, ps + lane * 16, valid);
+        if (lane < C::SB / 16) cp_async16z(st + u * EB + 2 * RB + lane * 16, ps, valid);
       }
     }
+    if constexpr (ES && PASS == 2) {  // (P, dP) of the stage's entries, stored in CSR order by the row pass
+      const int ku = lane / H, kh = lane % H;
+      const uint32_t ke = (uint32_t)__shfl_sync(kFull, wsrc, off + ku);
+      if (lane < U * H)
+        cp_async8z(st + U * EB + lane * 8,  // window entries past the item may be remote rows (src -1)
+                   row_addr(reinterpret_cast<const char*>(a.es_in) + kh * 8, ku < cnt ? ke : 0u, H * 8), ku < cnt);
+    }
+    md.e0 = pe;
     md.cnt = cnt;
     md.own = cur_own;
     md.first = cur_first;
@@ -429,9 +480,16 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
     if (cur_first) {
       char* o = owns + s * C::OWNP;
       const int64_t r = cur_own >= 0 ? cur_own : a.cown[-1 - (int64_t)cur_own];
-      cp_slice<LB>(o, a.oa + r * RB, lane);
-      if constexpr (PASS >= 1) cp_slice<LB>(o + RB, a.ob + r * RB, lane);
-      if constexpr (PASS == 1) cp_async<4>(o + 2 * RB + head * 4, a.lse + r * H + head);
+      if constexpr (PASS == 0) {
+        cp_slice<LB>(o, a.oa + r * RB, lane);
+      } else if constexpr (PASS == 1) {
+        cp_slice<LB>(o, a.oa + r * RB, lane);
+        cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
+        cp_async<4>(o + C::OWN_LSE + head * 4, a.lse + r * H + head);
+      } else if constexpr (!ES) {
+        cp_slice<LB>(o, a.oa + r * RB, lane);
+        cp_slice<LB>(o + RB, a.ob + r * RB, lane);
+      }
       cur_first = false;
     }
     pe += cnt;
@@ -468,16 +526,22 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
           l = 0.f;
         } else if constexpr (PASS == 1) {
           lds_f32<T, EPL>(o + lane * LB, q);
-          lds_raw<W>(o + RB + lane * LB, ow);
-          m = reinterpret_cast<const float*>(o + 2 * RB)[head] * kLog2e;
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
+          for (int i = 0; i < EPL; ++i) q[i] *= a.qscale;
+          lds_raw<W>(o + C::OWN_DY + lane * LB, ow);
+          m = reinterpret_cast<const float*>(o + C::OWN_LSE)[head] * kLog2e;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) { acc[i] = 0.f; acc2[i] = 0.f; }
           l = 0.f;
         } else {
-          lds_f32<T, EPL>(o + lane * LB, q);      // k_j
-          lds_f32<T, EPL>(o + RB + lane * LB, g); // v_j
+          if constexpr (!ES) {
+            lds_f32<T, EPL>(o + lane * LB, q);      // k_j
+            lds_f32<T, EPL>(o + RB + lane * LB, g); // v_j
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) { q[i] *= a.qscale; acc[i] = 0.f; acc2[i] = 0.f; }
+            for (int i = 0; i < EPL; ++i) q[i] *= a.qscale;
+          }
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) { acc[i] = 0.f; acc2[i] = 0.f; }
         }
       }
       const int cnt = cur.cnt;
@@ -515,10 +579,25 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
           const float s_ = head_sum<LPH>(dot<EPL>(q, kf));
           const float dp = head_sum<LPH>(dot_raw<T, W>(ow, vw));
           const float p = u < cnt ? ex2(s_ - m) : 0.f;
+          if constexpr (ES)  // all lanes of a head write the same 8 bytes
+            reinterpret_cast<float2*>(xs + s * C::XS)[u * H + head] = make_float2(p, dp);
           const float pd = p * dp;
           l += pd;
           axpy<EPL>(pd, kf, acc);
           axpy<EPL>(p, kf, acc2);
+        }
+        if constexpr (ES) {
+          // (P, dP)[entry e0 + u][head][2] of the stage, transposed through shared memory and written
+          // with one coalesced store per 32 values (the stage's scratch is rewritten two stages later,
+          // after another __syncwarp).  Masked neighbours go to a per-lane scratch slot past the array.
+          __syncwarp();
+          const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
+#pragma unroll
+          for (int t = 0; t < (2 * U * H + 31) / 32; ++t) {
+            const int f = lane + 32 * t;
+            const bool ok = f < 2 * U * H && f / (2 * H) < cnt;
+            a.es_out[ok ? cur.e0 * (2 * H) + f : a.es_scratch + lane] = x[f < 2 * U * H ? f : 0];
+          }
         }
       } else {
 #pragma unroll
@@ -527,9 +606,16 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
           lds_f32<T, EPL>(st + u * EB + lane * LB, qf);
           lds_f32<T, EPL>(st + u * EB + RB + lane * LB, gf);
           const float2 sd = reinterpret_cast<const float2*>(st + u * EB + 2 * RB)[head];
-          const float s_ = head_sum<LPH>(dot<EPL>(qf, q));
-          const float dp = head_sum<LPH>(dot<EPL>(gf, g));
-          const float p = u < cnt ? ex2(s_ - sd.x) : 0.f;
+          float p, dp;
+          if constexpr (ES) {  // stored by the row pass; zero-filled for masked neighbours
+            const float2 e = reinterpret_cast<const float2*>(st + U * EB)[u * H + head];
+            p = e.x;
+            dp = e.y;
+          } else {
+            const float s_ = head_sum<LPH>(dot<EPL>(qf, q));
+            dp = head_sum<LPH>(dot<EPL>(gf, g));
+            p = u < cnt ? ex2(s_ - sd.x) : 0.f;
+          }
           const float ds = p * (dp - sd.y);
           axpy<EPL>(p, gf, acc2);   // dV
           axpy<EPL>(ds, qf, acc);   // dK (unscaled)
@@ -582,13 +668,13 @@ __global__ void __launch_bounds__(kWarps * 32) pipe_kernel(PArgs a) {
 }
 
 // ----------------------------------------------------------------- launcher --
-template <typename T, int H, int D, int PASS, bool HALO>
+template <typename T, int H, int D, int PASS, bool HALO, bool ES>
 gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
-  using C = PC<T, H, D, PASS>;
+  using C = PC<T, H, D, PASS, ES>;
   static int grid = 0;
   const size_t smem = (size_t)kWarps * C::WARP_SMEM;
   if (!grid) {
-    auto k = pipe_kernel<T, H, D, PASS, HALO>;
+    auto k = pipe_kernel<T, H, D, PASS, HALO, ES>;
     GT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
@@ -607,7 +693,7 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
   }
   const int g = (int)std::min<int64_t>(cap, (want + kWarps - 1) / kWarps);
   GT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
-  pipe_kernel<T, H, D, PASS, HALO><<<g, kWarps * 32, smem, st>>>(a);
+  pipe_kernel<T, H, D, PASS, HALO, ES><<<g, kWarps * 32, smem, st>>>(a);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
 }
@@ -615,24 +701,29 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
 template <typename T, int H, int D>
 struct Ops {
   static gt_status run(int pass, const PArgs& a, cudaStream_t st, int rs) {
+    const bool es = a.es_out || a.es_in;
     if (a.halo) {
-      if (pass == 0) return launch<T, H, D, 0, true>(a, st, rs);
-      if (pass == 1) return launch<T, H, D, 1, true>(a, st, rs);
-      return launch<T, H, D, 2, true>(a, st, rs);
+      if (pass == 0) return launch<T, H, D, 0, true, false>(a, st, rs);
+      if (pass == 1) return es ? launch<T, H, D, 1, true, true>(a, st, rs) : launch<T, H, D, 1, true, false>(a, st, rs);
+      return launch<T, H, D, 2, true, false>(a, st, rs);
     }
-    if (pass == 0) return launch<T, H, D, 0, false>(a, st, rs);
-    if (pass == 1) return launch<T, H, D, 1, false>(a, st, rs);
-    return launch<T, H, D, 2, false>(a, st, rs);
+    if (pass == 0) return launch<T, H, D, 0, false, false>(a, st, rs);
+    if (pass == 1) return es ? launch<T, H, D, 1, false, true>(a, st, rs) : launch<T, H, D, 1, false, false>(a, st, rs);
+    return es ? launch<T, H, D, 2, false, true>(a, st, rs) : launch<T, H, D, 2, false, false>(a, st, rs);
   }
 };
 
 gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream_t st, int rs) {
 #define GT_CASE(TT, HH, DD) \
   if (H == HH && D == DD) return Ops<TT, HH, DD>::run(pass, a, st, rs);
+#ifdef GT_QUICK_ONE_SHAPE  // tooling: SASS inspection of the products shape only
+#define GT_HCASES(TT) GT_CASE(TT, 4, 256)
+#else
 #define GT_HCASES(TT)                                                                              \
   GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
   GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
   GT_CASE(TT, 8, 256) GT_CASE(TT, 8, 512)
+#endif
   if (dtype == GT_F32) { GT_HCASES(float) }
   else { GT_HCASES(__nv_bfloat16) }
 #undef GT_HCASES
@@ -646,7 +737,8 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
 // to `part`; their merges are launched by the caller).
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
                     const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
-                    const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms) {
+                    const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms,
+                    const EntryState& es) {
   pipe::PArgs a{};
   const bool rows = pass != 2;
   a.ibeg = w.d_beg.as<int64_t>();
@@ -673,6 +765,10 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.part = part;
   a.qscale = P->scale * pipe::kLog2e;
   a.scale = P->scale;
+  a.es_out = es.out;
+  a.es_in = es.in;
+  a.src = es.src;
+  a.es_scratch = (int64_t)P->nnz_local * P->heads * 2;
   return pipe::dispatch(P->dtype, P->heads, P->heads * P->d, pass, a, st, reserve_sms);
 }
 

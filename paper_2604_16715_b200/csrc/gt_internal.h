@@ -130,6 +130,18 @@ struct gt_plan_s {
   gt::DevBuf d_part_rowb;          // [row chunks, 2 D + heads]
   gt::DevBuf d_part_colb;          // [col chunks, 2 D]
 
+  // materialised entry state (opts.edge_state; Table 1 stores U per edge): the row
+  // pass writes (P, dP) per entry in CSR order, and the column pass gathers them through the
+  // CSC -> CSR entry map instead of recomputing q.k and dY.v per entry
+  bool es = false;
+  gt::DevBuf d_pd;                 // f32 [nnz_local][heads][2], local CSR order
+  gt::DevBuf d_src;                // int32 [nnz_in_local]: local CSR entry of the CSC position, -1 if remote row
+  // column pass with world > 1 and es: phase A = local-row entries (stored state, runs while the
+  // in-halo stats are exchanged), phase B = remote-row entries (recompute); split columns merged
+  bool col_split = false;
+  gt::WorkList w_colp[2];
+  gt::ChunkTable col_chunks;
+
   // multi-rank exchange
   gt::Comm* comm = nullptr;
   bool own_comm = true;
@@ -173,14 +185,22 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st);
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
-                          const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st);
+                          const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st,
+                          cudaEvent_t side_ready);
 bool shape_supported(int heads, int d, int dtype);
 int launches_fwd(const gt_plan_s* P);
 int launches_bwd(const gt_plan_s* P);
 
+// Materialised per-entry state of the ES kernels (all null: recompute kernels).
+struct EntryState {
+  float* out = nullptr;          // rowb: (P, dP) [nnz_local][heads][2], local CSR order
+  const float* in = nullptr;     // colb: the same array
+  const int32_t* src = nullptr;  // colb: local CSC position -> local CSR entry (-1: remote row)
+};
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
                     const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
-                    const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms);
+                    const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms,
+                    const EntryState& es = EntryState());
 
 // pack kernels (comm.cu)
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,
@@ -189,8 +209,12 @@ gt_status pack_stats(const float* stats, const int32_t* idx, int64_t rows, int64
                      cudaStream_t st);
 
 // graph (graph.cu)
+// d_src (optional, int32[nnz]): CSR entry index of each CSC position
 gt_status build_csc_device(const int64_t* d_row_ptr, const int32_t* d_col, int64_t n, int64_t nnz,
-                           int64_t* d_col_ptr, int32_t* d_row, cudaStream_t st);
+                           int64_t* d_col_ptr, int32_t* d_row, int32_t* d_src, cudaStream_t st);
+// d_out[p - p_lo] = src[p] - e_lo for CSC positions p in [p_lo, p_hi) whose CSR entry is in [e_lo, e_hi), else -1
+gt_status build_local_src(const int32_t* d_src, int64_t p_lo, int64_t p_hi, int64_t e_lo, int64_t e_hi,
+                          int32_t* d_out, cudaStream_t st);
 
 // host helpers (host.cpp)
 gt_status validate_csr(const int64_t* row_ptr, const int32_t* col_idx, int64_t n, int64_t nnz);

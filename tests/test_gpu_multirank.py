@@ -18,7 +18,7 @@ from tests._util import TOL, check_lse, inputs, normwise, to_f64, to_torch
 pytestmark = pytest.mark.gpu
 
 
-def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0):
+def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0):
     import torch
     import paper_2604_16715_b200 as gt
     n = len(rp) - 1
@@ -34,7 +34,7 @@ def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=
             torch.cuda.set_device(0)
             s = torch.cuda.Stream()
             plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, world=world, rank=r, comm=grp,
-                           strategy=strategy, heavy_threshold=heavy, partition=partition)
+                           strategy=strategy, heavy_threshold=heavy, partition=partition, edge_state=edge_state)
             lo, hi = plan.row_lo, plan.row_hi
             with torch.cuda.stream(s):
                 tq, tk, tv, tdy = (t[lo:hi].contiguous() for t in full)
@@ -89,14 +89,17 @@ def check(rp, ci, dtype, ins, res, world, partition=0):
         np.testing.assert_array_equal(ex["csc_idx"], ri[cp[lo]:cp[hi]])
 
 
+@pytest.mark.parametrize("edge_state", [1, -1])
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("strategy", ["halo", "allgather"])
-def test_loopback_directed_power_law(world, strategy):
+def test_loopback_directed_power_law(world, strategy, edge_state):
     rp, ci = gtgen.random_graph(2500, 30000, seed=70 + world, directed=True, power=2.1)
-    ins, res = run_loopback(rp, ci, 4, 64, "bf16", world, strategy, seed=700 + world, heavy=64)
+    ins, res = run_loopback(rp, ci, 4, 64, "bf16", world, strategy, seed=700 + world, heavy=64,
+                            edge_state=edge_state)
     check(rp, ci, "bf16", ins, res, world)
     for r in res:
         assert r[4]["strategy_name"] == strategy
+        assert r[4]["edge_state"] == (0 if edge_state < 0 else 1)
 
 
 def test_loopback_communities_f32_auto():

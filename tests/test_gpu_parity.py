@@ -22,14 +22,16 @@ def gt():
     return g
 
 
-def run_case(gt, row_ptr, col_idx, h, d, dtype, seed, scale=None, qk_scale=1.0, heavy=0, q_zero=False):
+def run_case(gt, row_ptr, col_idx, h, d, dtype, seed, scale=None, qk_scale=1.0, heavy=0, q_zero=False,
+             edge_state=0):
     import torch
     n = len(row_ptr) - 1
     q, k, v, dy = inputs(n, h, d, dtype, seed, qk_scale)
     if q_zero:
         q = np.zeros_like(q)
     scale = scale if scale is not None else 1.0 / math.sqrt(h * d)
-    plan = gt.Plan(row_ptr, col_idx, h, d, dtype=dtype, scale=scale, heavy_threshold=heavy)
+    plan = gt.Plan(row_ptr, col_idx, h, d, dtype=dtype, scale=scale, heavy_threshold=heavy, edge_state=edge_state)
+    assert plan.info()["edge_state"] == (0 if edge_state < 0 else 1)
     tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
     y, lse = plan.fwd(tq, tk, tv)
     dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy)
@@ -62,16 +64,19 @@ SHAPES = [  # h, d, dtype
 ]
 
 
+# edge_state 1: materialised logits and (P, dP) (default plan); -1: recompute kernels
+@pytest.mark.parametrize("edge_state", [1, -1])
 @pytest.mark.parametrize("h,d,dtype", SHAPES)
-def test_shapes_power_law_with_chunking(gt, h, d, dtype):
+def test_shapes_power_law_with_chunking(gt, h, d, dtype, edge_state):
     rp, ci = gtgen.random_graph(3000, 45000, seed=7 + h + d, directed=True, power=2.05)
-    run_case(gt, rp, ci, h, d, dtype, seed=200 + h * d, heavy=48)
+    run_case(gt, rp, ci, h, d, dtype, seed=200 + h * d, heavy=48, edge_state=edge_state)
 
 
+@pytest.mark.parametrize("edge_state", [1, -1])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_peaked_softmax_logits_x8(gt, dtype):
+def test_peaked_softmax_logits_x8(gt, dtype, edge_state):
     rp, ci = gtgen.random_graph(2000, 30000, seed=31, power=2.2)
-    run_case(gt, rp, ci, 4, 64, dtype, seed=301, scale=8.0 / math.sqrt(64), heavy=64)
+    run_case(gt, rp, ci, 4, 64, dtype, seed=301, scale=8.0 / math.sqrt(64), heavy=64, edge_state=edge_state)
 
 
 def test_all_equal_logits(gt):
@@ -89,13 +94,14 @@ def test_empty_graph_and_isolated_rows(gt):
     assert float(dk.abs().max()) == 0.0 and float(dv.abs().max()) == 0.0
 
 
-def test_single_edge_and_star(gt):
+@pytest.mark.parametrize("edge_state", [1, -1])
+def test_single_edge_and_star(gt, edge_state):
     rp, ci = gtgen.csr_from_pairs(5, [(3, 1)])
-    run_case(gt, rp, ci, 2, 64, "f32", seed=304)
+    run_case(gt, rp, ci, 2, 64, "f32", seed=304, edge_state=edge_state)
     n = 700  # hub row 0 -> all, all -> hub column 0: exercises chunked rows and chunked columns
     pairs = [(0, j) for j in range(1, n)] + [(j, 0) for j in range(1, n)]
     rp, ci = gtgen.csr_from_pairs(n, pairs)
-    plan, *_ = run_case(gt, rp, ci, 4, 64, "bf16", seed=305, heavy=100)
+    plan, *_ = run_case(gt, rp, ci, 4, 64, "bf16", seed=305, heavy=100, edge_state=edge_state)
     inf = plan.info()
     assert inf["heavy_rows"] == 1 and inf["heavy_cols"] == 1 and inf["heavy_row_chunks"] == 7
 
@@ -105,10 +111,11 @@ def test_one_row_single_node(gt):
     run_case(gt, rp, ci, 1, 128, "f32", seed=306)
 
 
-def test_csc_bitexact_and_deterministic(gt):
+@pytest.mark.parametrize("edge_state", [1, -1])
+def test_csc_bitexact_and_deterministic(gt, edge_state):
     import torch
     rp, ci = gtgen.random_graph(5000, 80000, seed=41, power=2.1)
-    plan, errs, ins, outs = run_case(gt, rp, ci, 4, 64, "bf16", seed=401, heavy=128)
+    plan, errs, ins, outs = run_case(gt, rp, ci, 4, 64, "bf16", seed=401, heavy=128, edge_state=edge_state)
     cp, ri = oracle.transpose(rp, ci)
     np.testing.assert_array_equal(plan.export("csc_ptr"), cp)
     np.testing.assert_array_equal(plan.export("csc_idx"), ri)
@@ -169,3 +176,6 @@ def test_errors_are_reported(gt):
     uc = unsorted[1][::-1].copy()
     with pytest.raises(gt.GTError):
         gt.Plan(unsorted[0], uc, 4, 64)
+    with pytest.raises(gt.GTError) as e:
+        gt.Plan(rp, ci, 4, 64, edge_state=2)
+    assert e.value.status == 1  # GT_EINVAL
