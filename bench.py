@@ -37,6 +37,8 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--strategy", default=None, help="auto|allgather|halo (world > 1)")
     ap.add_argument("--heavy", type=int, default=0, help="heavy row/column threshold (0 = library default)")
+    ap.add_argument("--edge-state", type=int, default=int(os.environ.get("GT_EDGE_STATE", "0")),
+                    help="gt_opts.edge_state: 0 auto (materialise when it fits), 1 on, -1 recompute")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -216,7 +218,8 @@ def run_ours(args):
     strategy = args.strategy or ("single" if world == 1 else "auto")
     t_plan = time.perf_counter()
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
-                   strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local)
+                   strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local,
+                   edge_state=args.edge_state)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     info = plan.info()
@@ -327,7 +330,8 @@ def run_ours(args):
             "config": {"workload": cfg.name, "nodes": n, "nnz": nnz, "heads": h, "head_dim": d,
                        "strategy": info["strategy_name"], "parallelism": f"graph-row x{world}",
                        "l2": "inputs larger than L2 (K, V tables 1.25 GB each vs 126 MB L2); no flush",
-                       "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 1024},
+                       "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 1024,
+                       "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"]},
             "roofline": roofline,
             "step_hbm_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
             "stages_ms": {s: stages[s][0] / max(stages[s][1], 1) for s in stages},

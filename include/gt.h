@@ -104,9 +104,10 @@ typedef struct {
   int edge_state;          /* per-entry state of the backward (Table 1 keeps U per edge,
                               P:166): 0 => materialise when it fits in 85 % of free device memory,
                               1 => materialise (GT_ENOMEM if it does not fit), -1 => never
-                              (recompute q.k and dY.v in the column pass).  Materialised, the row
-                              pass stores (P, dP) in fp32, 8 h B per owned-row entry, and the plan
-                              holds a 4 B CSC -> CSR map per owned-column entry. */
+                              (recompute q.k in the row pass, q.k and dY.v in the column pass).
+                              Materialised, the forward stores base-2 logits (4 h B per owned-row
+                              entry), the row pass (P, dP) (8 h B per owned-row entry), both fp32,
+                              and the plan holds a 4 B CSC -> CSR map per owned-column entry. */
 } gt_opts;
 
 typedef struct {

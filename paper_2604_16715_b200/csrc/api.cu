@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -200,8 +201,8 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
                            const gt_opts* opts, gt_plan_t* out) {
   if (!csr || !out || !opts) return fail(GT_EINVAL, "gt_plan: null argument");
   *out = nullptr;
-  if (n < 0 || nnz < 0 || n >= (1ll << 31) - 1 || nnz >= (1ll << 31) - 1)
-    return fail(GT_EINVAL, "gt_plan: n and nnz must be in [0, 2^31 - 1)");
+  if (n < 0 || nnz < 0 || n >= (1ll << 31) - 128 || nnz >= (1ll << 31) - 128)  // kernels index entries in 32 bits
+    return fail(GT_EINVAL, "gt_plan: n and nnz must be in [0, 2^31 - 128)");
   if (!csr->row_ptr || (nnz > 0 && !csr->col_idx)) return fail(GT_EINVAL, "gt_plan: null CSR arrays");
   if (heads <= 0 || d <= 0) return fail(GT_EINVAL, "gt_plan: heads and d must be positive");
   if (!shape_supported(heads, d, opts->dtype))
@@ -457,17 +458,21 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     // ---- materialised entry state (opts.edge_state) ----
     if (opts->edge_state < -1 || opts->edge_state > 1) return fail(GT_EINVAL, "gt_plan: edge_state must be -1, 0 or 1");
     if (opts->edge_state >= 0) {
-      const int64_t es_bytes = P->nnz_local * heads * 8 + P->nnz_in_local * 4;
+      const char* lg = std::getenv("GT_ES_LOGITS");  // logits half of the state (A/B switch; default on)
+      const bool logits = !(lg && lg[0] == '0');
+      const int64_t es_bytes = P->nnz_local * heads * (logits ? 12 : 8) + P->nnz_in_local * 4;
       size_t free_b = 0, total_b = 0;
       GT_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
       double misfit = (double)es_bytes < 0.85 * (double)free_b ? 0.0 : 1.0;
       if (!single) GT_TRY(P->comm->max_host(&misfit, st));  // the column-pass split must agree across ranks
       if (misfit > 0 && opts->edge_state == 1) return fail(GT_ENOMEM, "gt_plan: entry state does not fit in device memory");
       P->es = misfit == 0;
+      P->es_logits = P->es && logits;
       P->info.edge_state_bytes = P->es ? es_bytes : 0;
     }
     if (P->es) {
-      GT_TRY(P->d_pd.alloc(((size_t)P->nnz_local * heads * 2 + 32) * sizeof(float)));  // + masked-store scratch
+      if (P->es_logits) GT_TRY(P->d_s2.alloc(std::max<size_t>((size_t)P->nnz_local, 1) * heads * sizeof(float)));
+      GT_TRY(P->d_pd.alloc(std::max<size_t>((size_t)P->nnz_local, 1) * heads * 2 * sizeof(float)));
       GT_TRY(P->d_src.alloc(std::max<size_t>((size_t)P->nnz_in_local, 1) * sizeof(int32_t)));
       GT_TRY(build_local_src(full_src.as<int32_t>(), c0, c1, csr->row_ptr[P->lo], csr->row_ptr[P->hi],
                              P->d_src.as<int32_t>(), st));
@@ -526,7 +531,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
-                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_pd, &P->d_src})
+                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src})
     dev += (int64_t)b->bytes;
   I.device_bytes = dev;
   *out = P.release();

@@ -229,12 +229,16 @@ int launches_bwd(const gt_plan_s* P) {
   return rows + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_cols.nchunks() > 0 ? 1 : 0);
 }
 
-// Entry-state arguments of a pass (Table 1 keeps U per edge): the row pass stores
-// (P, dP) per entry in local CSR order; the column pass reads them through the CSC -> CSR map.
+// Entry-state arguments of a pass (Table 1 keeps Z and U per edge): the forward
+// stores base-2 logits and the row pass (P, dP) per entry in local CSR order; the row pass reads the
+// logits in the same order, the column pass reads (P, dP) through the CSC -> CSR map.
 static EntryState entry_state(gt_plan_s* P, int pass) {
   EntryState e;
   if (!P->es) return e;
-  if (pass == 1) {
+  if (pass == 0) {
+    if (P->es_logits) e.out = P->d_s2.as<float>();
+  } else if (pass == 1) {
+    if (P->es_logits) e.in = P->d_s2.as<float>();
     e.out = P->d_pd.as<float>();
   } else if (pass == 2) {
     e.in = P->d_pd.as<float>();
@@ -251,12 +255,14 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
   float* part = P->d_part_fwd.as<float>();
   const ChunkTable& ct = P->fwd_split ? P->fwd_chunks : P->heavy_rows;
   if (!P->fwd_split) {
-    GT_TRY(pipe_pass(P, 0, P->w_rows, ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0));
+    GT_TRY(pipe_pass(P, 0, P->w_rows, ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0,
+                     entry_state(P, 0)));
   } else {
     GT_TRY(pipe_pass(P, 0, P->w_fwd[0], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st,
-                     kReserveSms));
+                     kReserveSms, entry_state(P, 0)));
     if (halo_ready) GT_CUDA_TRY(cudaStreamWaitEvent(st, halo_ready, 0));
-    GT_TRY(pipe_pass(P, 0, P->w_fwd[1], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0));
+    GT_TRY(pipe_pass(P, 0, P->w_fwd[1], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0,
+                     entry_state(P, 0)));
   }
   if (ct.nchunks() > 0) {
     MergeArgs m = merge_args(ct, P->d_part_fwd, P->scale);

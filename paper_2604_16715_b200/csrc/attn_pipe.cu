@@ -65,6 +65,10 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool val
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 16 : 0)
                : "memory");
 }
+__device__ __forceinline__ void cp_async4z(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async8z(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(dst)), "l"(src), "r"(valid ? 8 : 0)
                : "memory");
@@ -81,6 +85,12 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// predicated global store (no branch, so the warp stays provably converged for the shuffles)
+__device__ __forceinline__ void st_pred(float* p, float x, bool on) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;}" ::"l"(p), "f"(x),
+               "r"((int)on) : "memory");
+}
+
 __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
   float2 d;
   asm("{.reg .b64 ra, rb, rc, rd;\n\t"
@@ -91,7 +101,7 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
   return d;
 }
 
-template <typename T, int H, int D, int PASS, bool ES>
+template <typename T, int H, int D, int PASS, int ES>
 struct PC {
   static constexpr int RB = D * (int)sizeof(T);          // bytes of one feature row
   static constexpr int EPL = D / 32;                      // elements per lane
@@ -103,13 +113,15 @@ struct PC {
   // pass stored and needs no own-column data)
   static constexpr int OWN_DY = PASS == 1 ? RB : 0;
   static constexpr int OWN_LSE = OWN_DY + RB;
-  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * H : (ES ? 0 : 2 * RB));
+  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * H : ((ES & 1) ? 0 : 2 * RB));
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
-  // per-stage entry state (ES column pass): (P, dP)[U][H] f32x2 gathered from the row pass's store
-  static constexpr int AUX = (ES && PASS == 2) ? U * H * 8 : 0;
+  // per-stage entry state gathered into the stage (ES): rowb s2[U][H] f32 (the forward's logits),
+  // colb (P, dP)[U][H] f32x2 (the row pass's)
+  static constexpr int AUX = PASS == 1 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 2 && (ES & 1)) ? U * H * 8 : 0);
   static constexpr int STAGE = (U * EB + AUX + 15) / 16 * 16;
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
-  static constexpr int XS = (ES && PASS == 1) ? U * H * 8 : 0;       // rowb ES: (P, dP) transpose scratch
+  // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dP)[U][H]
+  static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * 8 : 0);
   static constexpr int WARP_SMEM = kS * (STAGE + OWNP + XS);
   static_assert(LB == 8 || LB % 16 == 0, "lane slice must be 8 bytes or a multiple of 16");
   static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
@@ -140,9 +152,9 @@ struct PArgs {
   float* part;           // chunk partials
   float qscale, scale;
   // materialised entry state (ES kernels; Table 1 keeps U per edge)
-  float* es_out;         // rowb: (P, dP) [nnz_local][H][2] in local CSR entry order (+ 32 scratch floats)
-  int64_t es_scratch;    // rowb: float offset of the scratch slots (masked stores)
-  const float* es_in;    // colb: the same array
+  float* es_out;         // fwd: s2 [nnz_local][H] base-2 logits | rowb: (P, dP) [nnz_local][H][2], both
+                         // in local CSR entry order
+  const float* es_in;    // rowb: s2 | colb: (P, dP)
   const int32_t* src;    // colb: local CSC position -> local CSR entry (read through a window like nbr)
 };
 
@@ -307,21 +319,27 @@ __device__ __forceinline__ float head_sum(float x) {
 }
 
 struct Meta {      // warp-uniform description of one filled stage
-  int64_t e0;      // entry index (in `nbr` order) of the stage's first neighbour
+  int32_t e0;      // entry index (in `nbr` order) of the stage's first neighbour (nnz < 2^31)
   int32_t own;     // row/column id, or chunk -1 - c
   int32_t cnt;     // neighbours in the stage (0 = no work left)
   bool first, last;
 };
 
 // ------------------------------------------------------------------ kernel --
-// The ES row pass carries the stage entry offsets and the store pointer: hold it to 5 CTAs per SM
-// (<= 96 registers) where the lane slice is small enough not to spill.
-template <int PASS, bool ES, int EPL>
-constexpr int min_ctas() { return 1; }
+// Minimum resident CTAs per SM (register cap) of the backward passes where the lane slice is small
+// enough not to spill (A/B-tuned with tools/build_variants.py; 5 CTAs = 20 warps <= 96 registers).
+#ifndef GT_ROWB_MINB
+#define GT_ROWB_MINB 1
+#endif
+#ifndef GT_COLB_MINB
+#define GT_COLB_MINB 1
+#endif
+template <int PASS, int ES, int EPL>
+constexpr int min_ctas() { return EPL > 8 ? 1 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : 1)); }
 
-template <typename T, int H, int D, int PASS, bool HALO, bool ES>
+template <typename T, int H, int D, int PASS, bool HALO, int ES>
 __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) pipe_kernel(PArgs a) {
-  static_assert(!(ES && PASS == 2 && HALO), "the ES column pass reads local rows only");
+  static_assert(!((ES & 1) && PASS == 2 && HALO), "the ES column pass reads local rows only");
   using C = PC<T, H, D, PASS, ES>;
   constexpr int EPL = C::EPL, LPH = C::LPH, RB = C::RB, EB = C::EB, U = C::U, LB = C::LB;
   extern __shared__ __align__(128) char smem[];
@@ -333,14 +351,17 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
   char* const xs = owns + kS * C::OWNP;                      // kS * XS
 
   // ---------------- producer state (warp-uniform; per-lane only the tables) ----------------
-  int64_t t_next = 0, t_end = 0, batch_t0 = 0;
-  int64_t my_beg = 0, my_end = 0;    // lane k < kG: entry range of item batch_t0 + k
+  const int32_t nitems = (int32_t)a.nitems;
+  const int32_t nnbr = (int32_t)a.nnbr;
+  // entry and item indices are 32-bit (gt_plan: n, nnz < 2^31 - 1)
+  int32_t t_next = 0, t_end = 0, batch_t0 = 0;
+  int32_t my_beg = 0, my_end = 0;    // lane k < kG: entry range of item batch_t0 + k
   int32_t my_own = 0;                // lane k < kG: owner of item batch_t0 + k
   bool done = false;
-  int64_t pe = 0, pe_end = 0;        // current item's remaining edge range
+  int32_t pe = 0, pe_end = 0;        // current item's remaining edge range
   int32_t cur_own = 0;
   bool cur_first = false;
-  int64_t win_base = -(1ll << 40);   // lane l holds nbr[win_base + l] in win, nbr[win_base + 32 + l] in win_next
+  int32_t win_base = -(1 << 30);     // lane l holds nbr[win_base + l] in win, nbr[win_base + 32 + l] in win_next
   int32_t win = 0, win_next = 0;
   int32_t wsrc = 0, wsrc_next = 0;   // ES column pass: src[] over the same window
   // this lane's slice of row 0 of every gathered table: a row address is one mad.wide.u32
@@ -365,13 +386,13 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
     }
   };
 
-  auto load_window = [&](int64_t base) {
+  auto load_window = [&](int32_t base) {
     win_base = base;
-    win = (base + lane < a.nnbr) ? __ldg(a.nbr + base + lane) : 0;
-    win_next = (base + 32 + lane < a.nnbr) ? __ldg(a.nbr + base + 32 + lane) : 0;
-    if constexpr (ES && PASS == 2) {
-      wsrc = (base + lane < a.nnbr) ? __ldg(a.src + base + lane) : 0;
-      wsrc_next = (base + 32 + lane < a.nnbr) ? __ldg(a.src + base + 32 + lane) : 0;
+    win = (base + lane < nnbr) ? __ldg(a.nbr + base + lane) : 0;
+    win_next = (base + 32 + lane < nnbr) ? __ldg(a.nbr + base + 32 + lane) : 0;
+    if constexpr ((ES & 1) && PASS == 2) {
+      wsrc = (base + lane < nnbr) ? __ldg(a.src + base + lane) : 0;
+      wsrc_next = (base + 32 + lane < nnbr) ? __ldg(a.src + base + 32 + lane) : 0;
     }
   };
 
@@ -383,22 +404,22 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         unsigned long long b = 0;
         if (lane == 0) b = atomicAdd(a.counter, (unsigned long long)kG);
         b = __shfl_sync(kFull, b, 0);
-        if ((int64_t)b >= a.nitems) {
+        if ((int64_t)b >= nitems) {
           done = true;
           return false;
         }
-        batch_t0 = (int64_t)b;
-        t_end = min(batch_t0 + kG, a.nitems);
+        batch_t0 = (int32_t)b;
+        t_end = min(batch_t0 + kG, nitems);
         t_next = batch_t0;
-        const int64_t k = batch_t0 + lane;
-        const bool in = lane < kG && k < a.nitems;
-        my_beg = in ? __ldg(a.ibeg + k) : 0;
-        my_end = in ? __ldg(a.iend + k) : 0;
+        const int32_t k = batch_t0 + lane;
+        const bool in = lane < kG && k < nitems;
+        my_beg = in ? (int32_t)__ldg(a.ibeg + k) : 0;
+        my_end = in ? (int32_t)__ldg(a.iend + k) : 0;
         my_own = in ? __ldg(a.iown + k) : 0;
       }
       const int k = (int)(t_next - batch_t0);
-      const int64_t e0 = __shfl_sync(kFull, my_beg, k);
-      const int64_t e1 = __shfl_sync(kFull, my_end, k);
+      const int32_t e0 = __shfl_sync(kFull, my_beg, k);
+      const int32_t e1 = __shfl_sync(kFull, my_end, k);
       const int32_t own = __shfl_sync(kFull, my_own, k);
       ++t_next;
       if (e1 == e0) {
@@ -430,10 +451,10 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
     if (pe == win_base + 32) {  // slide the neighbour window; prefetch the one after
       win_base += 32;
       win = win_next;
-      win_next = (win_base + 32 + lane < a.nnbr) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
-      if constexpr (ES && PASS == 2) {
+      win_next = (win_base + 32 + lane < nnbr) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
+      if constexpr ((ES & 1) && PASS == 2) {
         wsrc = wsrc_next;
-        wsrc_next = (win_base + 32 + lane < a.nnbr) ? __ldg(a.src + win_base + 32 + lane) : 0;
+        wsrc_next = (win_base + 32 + lane < nnbr) ? __ldg(a.src + win_base + 32 + lane) : 0;
       }
     }
     const int off = (int)(pe - win_base);
@@ -465,7 +486,12 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         if (lane < C::SB / 16) cp_async16z(st + u * EB + 2 * RB + lane * 16, ps, valid);
       }
     }
-    if constexpr (ES && PASS == 2) {  // (P, dP) of the stage's entries, stored in CSR order by the row pass
+    if constexpr ((ES & 2) && PASS == 1) {  // s2 of the stage's entries (contiguous), stored by the forward
+      const bool kv = lane < cnt * H;
+      if (lane < U * H)
+        cp_async4z(st + U * EB + lane * 4, row_addr(reinterpret_cast<const char*>(a.es_in), (uint32_t)pe * H + (kv ? lane : 0), 4), kv);
+    }
+    if constexpr ((ES & 1) && PASS == 2) {  // (P, dP) of the stage's entries, stored in CSR order by the row pass
       const int ku = lane / H, kh = lane % H;
       const uint32_t ke = (uint32_t)__shfl_sync(kFull, wsrc, off + ku);
       if (lane < U * H)
@@ -483,10 +509,10 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       if constexpr (PASS == 0) {
         cp_slice<LB>(o, a.oa + r * RB, lane);
       } else if constexpr (PASS == 1) {
-        cp_slice<LB>(o, a.oa + r * RB, lane);
+        if constexpr (!(ES & 2)) cp_slice<LB>(o, a.oa + r * RB, lane);
         cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
         cp_async<4>(o + C::OWN_LSE + head * 4, a.lse + r * H + head);
-      } else if constexpr (!ES) {
+      } else if constexpr (!(ES & 1)) {
         cp_slice<LB>(o, a.oa + r * RB, lane);
         cp_slice<LB>(o + RB, a.ob + r * RB, lane);
       }
@@ -525,16 +551,18 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           m = -INFINITY;
           l = 0.f;
         } else if constexpr (PASS == 1) {
-          lds_f32<T, EPL>(o + lane * LB, q);
+          if constexpr (!(ES & 2)) {
+            lds_f32<T, EPL>(o + lane * LB, q);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) q[i] *= a.qscale;
+            for (int i = 0; i < EPL; ++i) q[i] *= a.qscale;
+          }
           lds_raw<W>(o + C::OWN_DY + lane * LB, ow);
           m = reinterpret_cast<const float*>(o + C::OWN_LSE)[head] * kLog2e;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) { acc[i] = 0.f; acc2[i] = 0.f; }
           l = 0.f;
         } else {
-          if constexpr (!ES) {
+          if constexpr (!(ES & 1)) {
             lds_f32<T, EPL>(o + lane * LB, q);      // k_j
             lds_f32<T, EPL>(o + RB + lane * LB, g); // v_j
 #pragma unroll
@@ -553,6 +581,12 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           lds_raw<W>(st + u * EB + lane * LB, kw);
           const float sv = head_sum<LPH>(dot_raw<T, W>(ow, kw)) * a.qscale;
           sc[u] = u < cnt ? sv : -INFINITY;
+          if constexpr (ES & 2) reinterpret_cast<float*>(xs + s * C::XS)[u * H + head] = sv;  // head lanes agree
+        }
+        if constexpr (ES & 2) {  // s2[entry e0 + u][head] for the row pass: one coalesced store per stage
+          __syncwarp();
+          const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
+          st_pred(a.es_out + (int64_t)cur.e0 * H + lane, x[lane < U * H ? lane : 0], lane < cnt * H);
         }
         float mx = m;
 #pragma unroll
@@ -576,27 +610,28 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           uint32_t vw[W];
           lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
           lds_raw<W>(st + u * EB + RB + lane * LB, vw);
-          const float s_ = head_sum<LPH>(dot<EPL>(q, kf));
+          float s_;
+          if constexpr (ES & 2) s_ = reinterpret_cast<const float*>(st + U * EB)[u * H + head];  // forward's logit
+          else s_ = head_sum<LPH>(dot<EPL>(q, kf));
           const float dp = head_sum<LPH>(dot_raw<T, W>(ow, vw));
           const float p = u < cnt ? ex2(s_ - m) : 0.f;
-          if constexpr (ES)  // all lanes of a head write the same 8 bytes
+          if constexpr (ES & 1)  // all lanes of a head write the same 8 bytes
             reinterpret_cast<float2*>(xs + s * C::XS)[u * H + head] = make_float2(p, dp);
           const float pd = p * dp;
           l += pd;
           axpy<EPL>(pd, kf, acc);
           axpy<EPL>(p, kf, acc2);
         }
-        if constexpr (ES) {
+        if constexpr (ES & 1) {
           // (P, dP)[entry e0 + u][head][2] of the stage, transposed through shared memory and written
           // with one coalesced store per 32 values (the stage's scratch is rewritten two stages later,
-          // after another __syncwarp).  Masked neighbours go to a per-lane scratch slot past the array.
+          // after another __syncwarp).
           __syncwarp();
           const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
 #pragma unroll
           for (int t = 0; t < (2 * U * H + 31) / 32; ++t) {
             const int f = lane + 32 * t;
-            const bool ok = f < 2 * U * H && f / (2 * H) < cnt;
-            a.es_out[ok ? cur.e0 * (2 * H) + f : a.es_scratch + lane] = x[f < 2 * U * H ? f : 0];
+            st_pred(a.es_out + (int64_t)cur.e0 * (2 * H) + f, x[f < 2 * U * H ? f : 0], f < 2 * cnt * H);
           }
         }
       } else {
@@ -607,7 +642,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           lds_f32<T, EPL>(st + u * EB + RB + lane * LB, gf);
           const float2 sd = reinterpret_cast<const float2*>(st + u * EB + 2 * RB)[head];
           float p, dp;
-          if constexpr (ES) {  // stored by the row pass; zero-filled for masked neighbours
+          if constexpr (ES & 1) {  // stored by the row pass; zero-filled for masked neighbours
             const float2 e = reinterpret_cast<const float2*>(st + U * EB)[u * H + head];
             p = e.x;
             dp = e.y;
@@ -668,7 +703,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 }
 
 // ----------------------------------------------------------------- launcher --
-template <typename T, int H, int D, int PASS, bool HALO, bool ES>
+template <typename T, int H, int D, int PASS, bool HALO, int ES>
 gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
   using C = PC<T, H, D, PASS, ES>;
   static int grid = 0;
@@ -700,16 +735,28 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
 
 template <typename T, int H, int D>
 struct Ops {
+  // ES bits: 1 = (P, dP) materialised (rowb stores, colb reads), 2 = logits materialised (fwd stores,
+  // rowb reads)
   static gt_status run(int pass, const PArgs& a, cudaStream_t st, int rs) {
-    const bool es = a.es_out || a.es_in;
-    if (a.halo) {
-      if (pass == 0) return launch<T, H, D, 0, true, false>(a, st, rs);
-      if (pass == 1) return es ? launch<T, H, D, 1, true, true>(a, st, rs) : launch<T, H, D, 1, true, false>(a, st, rs);
-      return launch<T, H, D, 2, true, false>(a, st, rs);
+    if (pass == 0) {
+      if (a.halo) return a.es_out ? launch<T, H, D, 0, true, 2>(a, st, rs) : launch<T, H, D, 0, true, 0>(a, st, rs);
+      return a.es_out ? launch<T, H, D, 0, false, 2>(a, st, rs) : launch<T, H, D, 0, false, 0>(a, st, rs);
     }
-    if (pass == 0) return launch<T, H, D, 0, false, false>(a, st, rs);
-    if (pass == 1) return es ? launch<T, H, D, 1, false, true>(a, st, rs) : launch<T, H, D, 1, false, false>(a, st, rs);
-    return es ? launch<T, H, D, 2, false, true>(a, st, rs) : launch<T, H, D, 2, false, false>(a, st, rs);
+    if (pass == 1) {
+      const int m = (a.es_out ? 1 : 0) | (a.es_in ? 2 : 0);
+      if (a.halo) {
+        if (m == 3) return launch<T, H, D, 1, true, 3>(a, st, rs);
+        if (m == 1) return launch<T, H, D, 1, true, 1>(a, st, rs);
+        if (m == 2) return launch<T, H, D, 1, true, 2>(a, st, rs);
+        return launch<T, H, D, 1, true, 0>(a, st, rs);
+      }
+      if (m == 3) return launch<T, H, D, 1, false, 3>(a, st, rs);
+      if (m == 1) return launch<T, H, D, 1, false, 1>(a, st, rs);
+      if (m == 2) return launch<T, H, D, 1, false, 2>(a, st, rs);
+      return launch<T, H, D, 1, false, 0>(a, st, rs);
+    }
+    if (a.halo) return launch<T, H, D, 2, true, 0>(a, st, rs);
+    return a.es_in ? launch<T, H, D, 2, false, 1>(a, st, rs) : launch<T, H, D, 2, false, 0>(a, st, rs);
   }
 };
 
@@ -768,7 +815,6 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.es_out = es.out;
   a.es_in = es.in;
   a.src = es.src;
-  a.es_scratch = (int64_t)P->nnz_local * P->heads * 2;
   return pipe::dispatch(P->dtype, P->heads, P->heads * P->d, pass, a, st, reserve_sms);
 }
 

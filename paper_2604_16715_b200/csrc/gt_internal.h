@@ -134,6 +134,8 @@ struct gt_plan_s {
   // pass writes (P, dP) per entry in CSR order, and the column pass gathers them through the
   // CSC -> CSR entry map instead of recomputing q.k and dY.v per entry
   bool es = false;
+  bool es_logits = false;          // the forward's logits are part of the state (GT_ES_LOGITS, default 1)
+  gt::DevBuf d_s2;                 // f32 [nnz_local][heads] base-2 logits of the forward, local CSR order
   gt::DevBuf d_pd;                 // f32 [nnz_local][heads][2], local CSR order
   gt::DevBuf d_src;                // int32 [nnz_in_local]: local CSR entry of the CSC position, -1 if remote row
   // column pass with world > 1 and es: phase A = local-row entries (stored state, runs while the
@@ -193,8 +195,8 @@ int launches_bwd(const gt_plan_s* P);
 
 // Materialised per-entry state of the ES kernels (all null: recompute kernels).
 struct EntryState {
-  float* out = nullptr;          // rowb: (P, dP) [nnz_local][heads][2], local CSR order
-  const float* in = nullptr;     // colb: the same array
+  float* out = nullptr;          // fwd: s2 [nnz_local][heads] | rowb: (P, dP) [nnz_local][heads][2]
+  const float* in = nullptr;     // rowb: s2 | colb: (P, dP)
   const int32_t* src = nullptr;  // colb: local CSC position -> local CSR entry (-1: remote row)
 };
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
