@@ -21,5 +21,7 @@ for i in ${PASSES:-0 1 2}; do
   ncu -i /tmp/prof_pass$i.ncu-rep --page raw --csv > gpurun_out/raw_pass$i.csv 2>&1
   ncu -i /tmp/prof_pass$i.ncu-rep --page source --csv --print-source sass > gpurun_out/src_pass$i.csv 2>&1
 done
+python tools/make_traffic.py C3-products fwd=/tmp/prof_pass0.ncu-rep bwd_rows=/tmp/prof_pass1.ncu-rep bwd_cols=/tmp/prof_pass2.ncu-rep > gpurun_out/traffic.log 2>&1
+cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
 du -sh gpurun_out
 echo done
