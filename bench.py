@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--heavy", type=int, default=0, help="heavy row/column threshold (0 = library default)")
     ap.add_argument("--edge-state", type=int, default=int(os.environ.get("GT_EDGE_STATE", "0")),
                     help="gt_opts.edge_state: 0 auto (materialise when it fits), 1 on, -1 recompute")
+    ap.add_argument("--bwd-mode", type=int, default=0,
+                    help="gt_opts.bwd_mode (world > 1): 0 transposed owner, 1 reduce-scatter of fp32 partials")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -219,7 +221,7 @@ def run_ours(args):
     t_plan = time.perf_counter()
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
                    strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local,
-                   edge_state=args.edge_state)
+                   edge_state=args.edge_state, bwd_mode=args.bwd_mode)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     info = plan.info()
@@ -331,7 +333,8 @@ def run_ours(args):
                        "strategy": info["strategy_name"], "parallelism": f"graph-row x{world}",
                        "l2": "inputs larger than L2 (K, V tables 1.25 GB each vs 126 MB L2); no flush",
                        "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 1024,
-                       "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"]},
+                       "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
+                       "bwd_mode": info["bwd_mode"]},
             "roofline": roofline,
             "step_hbm_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
             "stages_ms": {s: stages[s][0] / max(stages[s][1], 1) for s in stages},

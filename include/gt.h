@@ -108,6 +108,13 @@ typedef struct {
                               Materialised, the forward stores base-2 logits (4 h B per owned-row
                               entry), the row pass (P, dP) (8 h B per owned-row entry), both fp32,
                               and the plan holds a 4 B CSC -> CSR map per owned-column entry. */
+  int bwd_mode;            /* world > 1 backward dataflow (reading Z11 of PAPER.md P:113):
+                              0 => transposed owner: the owner of column j computes dK_j, dV_j after
+                                   receiving q || dY || (LSE, D) of its remote in-neighbour rows;
+                              1 => reduce-scatter (paper-faithful): every rank computes fp32 partial
+                                   dK || dV of the remote columns its rows touch and sends them to the
+                                   owners (all-gather: a reduce-scatter; halo: the reverse halo), which
+                                   sum them in a fixed order.  2 D fp32 per exchanged row. */
 } gt_opts;
 
 typedef struct {
@@ -132,6 +139,7 @@ typedef struct {
   double alpha_s_per_unit;        /* cost-model compute seconds per (edge + row) */
   int edge_state;                 /* 1 if the plan materialises per-entry state (gt_opts.edge_state) */
   int64_t edge_state_bytes;       /* device bytes of that state */
+  int bwd_mode;                   /* backward dataflow in use (gt_opts.bwd_mode; 0 when world == 1) */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,

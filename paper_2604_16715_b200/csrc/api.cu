@@ -144,6 +144,34 @@ static void make_ag_pattern(const gt_plan_s* P, Pattern& pt) {
 
 static int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
 
+// The forward pattern reversed, for the reduce-scatter backward: every received row (halo slot, or
+// padded all-gather block row) goes back to its owner as an fp32 partial.  send_idx of the result
+// holds, per received row, the local column it belongs to (-1: all-gather padding).
+static Pattern reverse_pattern(const gt_plan_s* P, const Pattern& f, bool ag) {
+  const int w = P->world;
+  Pattern r;
+  r.send_off = f.recv_off;
+  r.send_cnt = f.recv_cnt;
+  r.recv_off.assign(w, 0);
+  r.recv_cnt.assign(w, 0);
+  if (ag) {
+    r.send_idx.assign((size_t)w * P->n_max, -1);
+    for (int s = 0; s < w; ++s) {
+      r.recv_off[s] = (int64_t)s * P->n_max;
+      r.recv_cnt[s] = s == P->rank ? 0 : P->n_max;
+      if (s == P->rank) continue;
+      for (int64_t k = 0; k < P->n_local; ++k) r.send_idx[(size_t)(s * P->n_max + k)] = (int32_t)k;
+    }
+    r.recv_rows = (int64_t)w * P->n_max;
+  } else {
+    r.recv_off = f.send_off;
+    r.recv_cnt = f.send_cnt;
+    r.send_idx = f.send_idx;
+    r.recv_rows = (int64_t)f.send_idx.size();
+  }
+  return r;
+}
+
 }  // namespace gt
 
 using namespace gt;
@@ -180,6 +208,101 @@ gt_plan_s::~gt_plan_s() {
   if (comm && own_comm) delete comm;
 }
 
+static bool ag_of(const gt_plan_s* P) { return P->strategy == GT_ALLGATHER; }
+
+// Reduce-scatter backward structures (reading Z11):
+//  * halo columns: the local CSR's remote-column entries grouped by receive slot, rows ascending
+//    (d_hrow local row, d_hsrc local CSR entry); one work item per <= T-entry piece, all chunks;
+//  * owned columns over owned-row entries; a column with remote in-edges is always merged;
+//  * the reversed forward pattern, and per merged column the fixed-order list of rows to sum
+//    (its own pieces, then the received partials in rank order).
+static gt_status build_reduce_backward(gt_plan_s* P, const gt_csr* csr, const std::vector<int64_t>& rp_local,
+                                       const std::vector<int32_t>& cols, const DevBuf& full_row, int64_t c0, bool ag,
+                                       const Pattern& f, int64_t T, cudaStream_t st) {
+  (void)st;
+  const int64_t D = (int64_t)P->heads * P->d;
+  const int64_t nl = P->n_local;
+  P->rs_row_bytes = 2 * D * 4;
+  const int64_t nslots = f.recv_rows;
+  P->n_slots = nslots;
+  std::vector<int64_t> hptr((size_t)nslots + 1, 0);
+  for (int32_t c : cols)
+    if (c >= nl) ++hptr[(size_t)(c - nl) + 1];
+  for (int64_t s = 0; s < nslots; ++s) hptr[s + 1] += hptr[s];
+  P->n_hent = hptr[nslots];
+  std::vector<int32_t> hrow((size_t)P->n_hent), hsrc((size_t)P->n_hent);
+  std::vector<int64_t> fill(hptr.begin(), hptr.end() - 1);
+  for (int64_t r = 0; r < nl; ++r)
+    for (int64_t e = rp_local[r]; e < rp_local[r + 1]; ++e) {
+      const int32_t c = cols[(size_t)e];
+      if (c < nl) continue;
+      const int64_t k = fill[(size_t)(c - nl)]++;
+      hrow[(size_t)k] = (int32_t)r;
+      hsrc[(size_t)k] = (int32_t)e;
+    }
+  GT_TRY(upload(P->d_hrow, hrow.data(), hrow.size()));
+  GT_TRY(upload(P->d_hsrc, hsrc.data(), hsrc.size()));
+  build_work(nslots, [&](int64_t s, std::vector<Segment>& o) { o.push_back({hptr[s], hptr[s + 1], 0}); }, T, 1,
+             &P->w_hcols, &P->hcol_chunks, [](int64_t) { return true; });
+  // owned columns, owned-row entries [e0 + a, e0 + b) (CSC rows ascend within a column)
+  std::vector<int32_t> grow((size_t)P->nnz_in_local);
+  if (P->nnz_in_local)
+    GT_CUDA_TRY(cudaMemcpy(grow.data(), full_row.as<int32_t>() + c0, grow.size() * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost));
+  std::vector<int64_t> la((size_t)nl), lb((size_t)nl);
+  for (int64_t c = 0; c < nl; ++c) {
+    const int32_t* r0 = grow.data() + P->h_col_ptr[c];
+    const int32_t* r1 = grow.data() + P->h_col_ptr[c + 1];
+    la[c] = std::lower_bound(r0, r1, (int32_t)P->lo) - r0;
+    lb[c] = std::lower_bound(r0, r1, (int32_t)P->hi) - r0;
+  }
+  build_work(nl,
+             [&](int64_t c, std::vector<Segment>& o) {
+               o.push_back({P->h_col_ptr[c] + la[c], P->h_col_ptr[c] + lb[c], 0});
+             },
+             T, 1, &P->w_colrs, &P->rs_chunks,
+             [&](int64_t c) { return la[c] > 0 || lb[c] < P->h_col_ptr[c + 1] - P->h_col_ptr[c]; });
+  for (ChunkTable* t : {&P->hcol_chunks, &P->rs_chunks}) {  // ids / first even when there are no pieces
+    GT_TRY(upload(t->d_ids, t->ids.data(), t->ids.size()));
+    GT_TRY(upload(t->d_first, t->first.data(), t->first.size()));
+    GT_TRY(upload(t->d_lo, t->chunk_lo.data(), t->chunk_lo.size()));
+    GT_TRY(upload(t->d_hi, t->chunk_hi.data(), t->chunk_hi.size()));
+    GT_TRY(upload(t->d_owner, t->chunk_owner.data(), t->chunk_owner.size()));
+  }
+  GT_TRY(upload_work(P->w_hcols));
+  GT_TRY(upload_work(P->w_colrs));
+  // reversed pattern and merge lists
+  const Pattern rev = reverse_pattern(P, f, ag);
+  P->rs_send_off = rev.send_off; P->rs_send_cnt = rev.send_cnt;
+  P->rs_recv_off = rev.recv_off; P->rs_recv_cnt = rev.recv_cnt;
+  P->rs_recv_rows = rev.recv_rows;
+  const int64_t nrc = P->rs_chunks.nchunks();
+  std::vector<int64_t> rptr((size_t)nl + 1, 0);
+  for (int32_t col : rev.send_idx)
+    if (col >= 0) ++rptr[(size_t)col + 1];
+  for (int64_t c = 0; c < nl; ++c) rptr[c + 1] += rptr[c];
+  std::vector<int64_t> rrows((size_t)rptr[nl]);
+  {
+    std::vector<int64_t> at(rptr.begin(), rptr.end() - 1);
+    for (int64_t k = 0; k < (int64_t)rev.send_idx.size(); ++k)  // ascending k = ascending rank
+      if (rev.send_idx[(size_t)k] >= 0) rrows[(size_t)at[(size_t)rev.send_idx[(size_t)k]]++] = k;
+  }
+  const auto& ids = P->rs_chunks.ids;
+  std::vector<int64_t> mptr(ids.size() + 1, 0), midx;
+  for (size_t x = 0; x < ids.size(); ++x) {
+    for (int32_t ch = P->rs_chunks.first[x]; ch < P->rs_chunks.first[x + 1]; ++ch) midx.push_back(ch);
+    for (int64_t k = rptr[(size_t)ids[x]]; k < rptr[(size_t)ids[x] + 1]; ++k) midx.push_back(nrc + rrows[(size_t)k]);
+    mptr[x + 1] = (int64_t)midx.size();
+  }
+  GT_TRY(upload(P->d_mptr, mptr.data(), mptr.size()));
+  GT_TRY(upload(P->d_midx, midx.data(), midx.size()));
+  GT_TRY(P->d_part_h.alloc((size_t)std::max<int64_t>(P->hcol_chunks.nchunks(), 1) * P->rs_row_bytes));
+  GT_TRY(P->d_rs_send.alloc((size_t)std::max<int64_t>(nslots, 1) * P->rs_row_bytes));
+  GT_TRY(P->d_part_rs.alloc((size_t)std::max<int64_t>(nrc + rev.recv_rows, 1) * P->rs_row_bytes));
+  (void)csr;
+  return GT_OK;
+}
+
 extern "C" {
 
 const char* gt_last_error(void) { return g_err.c_str(); }
@@ -214,6 +337,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   if (world == 1 && (opts->strategy == GT_ALLGATHER || opts->strategy == GT_HALO))
     return fail(GT_ECONFIG, "gt_plan: multi-GPU strategy requested with world == 1");
   if (opts->partition != 0 && opts->partition != 1) return fail(GT_EINVAL, "gt_plan: partition must be 0 or 1");
+  if (opts->bwd_mode != 0 && opts->bwd_mode != 1) return fail(GT_EINVAL, "gt_plan: bwd_mode must be 0 or 1");
   if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
   if (opts->validate) GT_TRY(validate_csr(csr->row_ptr, csr->col_idx, n, nnz));
   else if (csr->row_ptr[n] != nnz) return fail(GT_EGRAPH, "row_ptr[n] != nnz");
@@ -233,6 +357,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   P->scale = opts->scale > 0.f ? opts->scale : (float)(1.0 / std::sqrt((double)heads * d));
   P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 1024;
   P->profile = opts->profile != 0;
+  P->bwd_reduce = world > 1 && opts->bwd_mode == 1;
   P->stats_stride = (int)((8 * heads + 15) / 16 * 16 / 4);
   const int64_t D = (int64_t)heads * d;
   const int elt = opts->dtype == GT_F32 ? 4 : 2;
@@ -314,12 +439,17 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     P->info.alpha_s_per_unit = alpha;
     size_t free_b = 0, total_b = 0;
     GT_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const int64_t rs_bytes = 2 * D * 4;  // one fp32 partial dK || dV row (reduce-scatter backward)
     for (int c : {(int)GT_ALLGATHER, (int)GT_HALO}) {
       const Pattern& f = c == GT_ALLGATHER ? pf_ag : pf_halo;
-      const Pattern& b = c == GT_ALLGATHER ? pb_ag : pb_halo;
-      int64_t need = f.recv_rows * P->kv_row_bytes + b.recv_rows * P->in_row_bytes +
-                     std::max((int64_t)f.send_idx.size() * P->kv_row_bytes, (int64_t)b.send_idx.size() * P->in_row_bytes) +
-                     (c == GT_ALLGATHER ? P->n_max * (P->kv_row_bytes + P->in_row_bytes) : 0);
+      const Pattern rev = P->bwd_reduce ? reverse_pattern(P.get(), f, c == GT_ALLGATHER) : Pattern();
+      const Pattern& b = P->bwd_reduce ? rev : (c == GT_ALLGATHER ? pb_ag : pb_halo);
+      const int64_t b_row = P->bwd_reduce ? rs_bytes : P->in_row_bytes;
+      int64_t need = f.recv_rows * P->kv_row_bytes + b.recv_rows * b_row +
+                     (P->bwd_reduce ? f.recv_rows * 2 * rs_bytes
+                                    : std::max((int64_t)f.send_idx.size() * P->kv_row_bytes,
+                                               (int64_t)b.send_idx.size() * P->in_row_bytes) +
+                                          (c == GT_ALLGATHER ? P->n_max * (P->kv_row_bytes + P->in_row_bytes) : 0));
       double misfit = (double)need < 0.85 * (double)free_b ? 0.0 : 1.0;
       GT_TRY(P->comm->max_host(&misfit, st));  // every rank must agree (the probe below is collective)
       const double fits = misfit > 0 ? 0.0 : 1.0;
@@ -328,11 +458,11 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
         // measure the forward and backward exchanges of this pattern (2 warm-up + 3 timed)
         DevBuf sb, rf, rb;
         int64_t sbytes = std::max({(int64_t)f.send_idx.size() * P->kv_row_bytes,
-                                   (int64_t)b.send_idx.size() * P->in_row_bytes,
+                                   P->bwd_reduce ? f.recv_rows * rs_bytes : (int64_t)b.send_idx.size() * P->in_row_bytes,
                                    c == GT_ALLGATHER ? P->n_max * P->in_row_bytes : 0, (int64_t)16});
         GT_TRY(sb.alloc((size_t)sbytes));
         GT_TRY(rf.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
-        GT_TRY(rb.alloc((size_t)std::max<int64_t>(b.recv_rows * P->in_row_bytes, 16)));
+        GT_TRY(rb.alloc((size_t)std::max<int64_t>(b.recv_rows * b_row, 16)));
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -340,15 +470,15 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
         for (int it = 0; it < 5; ++it) {
           GT_TRY(P->comm->barrier(st));
           cudaEventRecord(e0, st);
-          if (c == GT_ALLGATHER) {
-            GT_TRY(P->comm->all_gather(sb.p, rf.p, P->n_max, P->kv_row_bytes, st));
-            GT_TRY(P->comm->all_gather(sb.p, rb.p, P->n_max, P->in_row_bytes, st));
-          } else {
+          if (c == GT_ALLGATHER) GT_TRY(P->comm->all_gather(sb.p, rf.p, P->n_max, P->kv_row_bytes, st));
+          else
             GT_TRY(P->comm->exchange(sb.p, f.send_off.data(), f.send_cnt.data(), rf.p, f.recv_off.data(),
                                      f.recv_cnt.data(), P->kv_row_bytes, st));
+          if (c == GT_ALLGATHER && !P->bwd_reduce)
+            GT_TRY(P->comm->all_gather(sb.p, rb.p, P->n_max, P->in_row_bytes, st));
+          else
             GT_TRY(P->comm->exchange(sb.p, b.send_off.data(), b.send_cnt.data(), rb.p, b.recv_off.data(),
-                                     b.recv_cnt.data(), P->in_row_bytes, st));
-          }
+                                     b.recv_cnt.data(), b_row, st));
           cudaEventRecord(e1, st);
           GT_CUDA_TRY(cudaEventSynchronize(e1));
           float ms = 0;
@@ -380,9 +510,10 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   }
 
   // ---- remapped local CSR columns and CSC rows ----
+  std::vector<int32_t> cols;  // remapped local CSR columns (kept for the reduce-scatter halo columns)
   if (!single) {
     const bool ag = P->strategy == GT_ALLGATHER;
-    std::vector<int32_t> cols(csr->col_idx + csr->row_ptr[P->lo], csr->col_idx + csr->row_ptr[P->hi]);
+    cols.assign(csr->col_idx + csr->row_ptr[P->lo], csr->col_idx + csr->row_ptr[P->hi]);
     remap_ids(cols.data(), (int64_t)cols.size(), P.get(), P->halo_out, ag);
     GT_TRY(upload(P->d_col, cols.data(), cols.size()));
     std::vector<int32_t> rows((size_t)P->nnz_in_local);
@@ -406,9 +537,11 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     if (ag) sbytes = P->n_max * P->kv_row_bytes;
     GT_TRY(P->d_send_buf.alloc((size_t)std::max<int64_t>(sbytes, 16)));
     GT_TRY(P->d_recv_kv.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
-    GT_TRY(P->d_recv_qd.alloc((size_t)std::max<int64_t>(b.recv_rows * P->kv_row_bytes, 16)));
-    GT_TRY(P->d_recv_st.alloc((size_t)std::max<int64_t>(b.recv_rows * P->st_row_bytes, 16)));
-    GT_TRY(P->d_send_st.alloc((size_t)std::max<int64_t>((ag ? P->n_max : (int64_t)b.send_idx.size()) * P->st_row_bytes, 16)));
+    if (!P->bwd_reduce) {  // transposed-owner backward: [q | dy] and (LSE2, D) rows of the in-halo
+      GT_TRY(P->d_recv_qd.alloc((size_t)std::max<int64_t>(b.recv_rows * P->kv_row_bytes, 16)));
+      GT_TRY(P->d_recv_st.alloc((size_t)std::max<int64_t>(b.recv_rows * P->st_row_bytes, 16)));
+      GT_TRY(P->d_send_st.alloc((size_t)std::max<int64_t>((ag ? P->n_max : (int64_t)b.send_idx.size()) * P->st_row_bytes, 16)));
+    }
     GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_bwd0, cudaEventDisableTiming));
     GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_rows, cudaEventDisableTiming));
     GT_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_side, cudaEventDisableTiming));
@@ -422,6 +555,17 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     P->info.exch_bwd_bytes = recv_b * P->in_row_bytes;
     P->info.send_fwd_bytes = send_f * P->kv_row_bytes;
     P->info.send_bwd_bytes = send_b * P->in_row_bytes;
+    if (P->bwd_reduce) {
+      const Pattern rev = reverse_pattern(P.get(), f, ag);
+      int64_t rs_recv = 0, rs_send = 0;
+      for (int s = 0; s < world; ++s) {
+        if (s == P->rank) continue;
+        rs_recv += rev.recv_cnt[s];
+        rs_send += rev.send_cnt[s];
+      }
+      P->info.exch_bwd_bytes = rs_recv * 2 * D * 4;
+      P->info.send_bwd_bytes = rs_send * 2 * D * 4;
+    }
   }
 
   // ---- degree binning and work lists (rows / columns split into chunks) ----
@@ -476,7 +620,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       GT_TRY(P->d_src.alloc(std::max<size_t>((size_t)P->nnz_in_local, 1) * sizeof(int32_t)));
       GT_TRY(build_local_src(full_src.as<int32_t>(), c0, c1, csr->row_ptr[P->lo], csr->row_ptr[P->hi],
                              P->d_src.as<int32_t>(), st));
-      if (!single) {
+      if (!single && !P->bwd_reduce) {
         // column split: CSC rows ascend within a column, so entries [e0, a) and [b, e1) have remote
         // rows (global row < lo or >= hi), [a, b) owned rows
         P->col_split = true;
@@ -501,6 +645,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
         for (auto* w : {&P->w_colp[0], &P->w_colp[1]}) GT_TRY(upload_work(*w));
       }
     }
+    // ---- reduce-scatter backward (opts.bwd_mode = 1) ----
+    if (P->bwd_reduce) GT_TRY(build_reduce_backward(P.get(), csr, rp_local, cols, full_row, c0, ag_of(P.get()),
+                                                    P->strategy == GT_ALLGATHER ? pf_ag : pf_halo, T, st));
     P->info.edge_state = P->es ? 1 : 0;
     GT_TRY(upload_chunks(P->heavy_rows));
     GT_TRY(upload_chunks(P->heavy_cols));
@@ -527,11 +674,13 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   I.heavy_cols = (int64_t)P->heavy_cols.ids.size();
   I.heavy_col_chunks = ncc;
   I.launches_fwd = launches_fwd(P.get()) + (single ? 0 : 1);
-  I.launches_bwd = launches_bwd(P.get()) + (single ? 0 : 1);
+  I.launches_bwd = launches_bwd(P.get()) + (single ? 0 : (P->bwd_reduce ? 0 : 1));
+  I.bwd_mode = P->bwd_reduce ? 1 : 0;
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
-                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src})
+                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src, &P->d_hrow,
+                          &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx})
     dev += (int64_t)b->bytes;
   I.device_bytes = dev;
   *out = P.release();
@@ -664,6 +813,26 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   const bool multi = P->world > 1;
   const bool ag = P->strategy == GT_ALLGATHER;
+  if (multi && P->bwd_reduce) {
+    // Reduce-scatter backward (reading Z11): row pass; fp32 partials of the halo columns, sent to their
+    // owners on the side stream while the owned columns run; then the fixed-order merge.
+    P->mark_begin(2, st, &ev);
+    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
+    GT_TRY(launch_bwd_halo_cols(P, q, dy, st));
+    P->mark_end(2, st, ev);
+    GT_CUDA_TRY(cudaEventRecord(P->ev_rows, st));
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_rows, 0));
+    P->mark_begin(3, P->side, &ev2);
+    char* recv = (char*)P->d_part_rs.p + P->rs_chunks.nchunks() * P->rs_row_bytes;
+    GT_TRY(P->comm->exchange(P->d_rs_send.p, P->rs_send_off.data(), P->rs_send_cnt.data(), recv,
+                             P->rs_recv_off.data(), P->rs_recv_cnt.data(), P->rs_row_bytes, P->side));
+    P->mark_end(3, P->side, ev2);
+    GT_CUDA_TRY(cudaEventRecord(P->ev_side, P->side));
+    P->mark_begin(4, st, &ev);
+    GT_TRY(launch_bwd_cols_rs(P, q, k, v, dy, dk, dv, st, P->ev_side));
+    P->mark_end(4, st, ev);
+    return GT_OK;
+  }
   if (multi) {
     // Side stream, overlapped with the row pass: [q | dy] rows of the in-halo are known at entry.
     // Both messages go on the side stream so the communicator sees one ordered sequence.

@@ -160,6 +160,56 @@ __global__ void __launch_bounds__(kBlock) colb_merge_kernel(MergeArgs a) {
   }
 }
 
+// Reduce-scatter backward, sender side: row `slot` of `out` = sum of the partial rows of its pieces
+// [first[slot], first[slot + 1]) in piece order (zeros for a slot without entries).  Rows: 2 D fp32.
+__global__ void __launch_bounds__(kBlock) sum_slots_kernel(int64_t nslots, const int32_t* first, const float4* part,
+                                                           int64_t row4, float4* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nslots; x += nw) {
+    const int c0 = first[x], c1 = first[x + 1];
+    for (int64_t i = lane; i < row4; i += 32) {
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = c0; c < c1; ++c) {
+        const float4 v = part[(int64_t)c * row4 + i];
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+      }
+      out[x * row4 + i] = s;
+    }
+  }
+}
+
+// Reduce-scatter backward, owner side: column ids[x] = the sum, in list order, of rows idx[ptr[x] ..
+// ptr[x + 1]) of `part` (its owned-row pieces first, then the partials received from each peer in
+// rank order): dK = scale * sum dK_c, dV = sum dV_c.
+template <typename T, int H, int D>
+__global__ void __launch_bounds__(kBlock) colb_merge_list_kernel(int64_t nids, const int32_t* ids, const int64_t* ptr,
+                                                                 const int64_t* idx, const float* part, char* dk,
+                                                                 char* dv, float scale) {
+  using C = Cfg<T, H, D>;
+  constexpr int EPL = C::EPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < nids; x += nw) {
+    const int64_t col = ids[x];
+    float K[EPL], V[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) { K[i] = 0.f; V[i] = 0.f; }
+    for (int64_t k = ptr[x]; k < ptr[x + 1]; ++k) {
+      const float* pp = part + idx[k] * (int64_t)(2 * D);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        K[i] += pp[lane * EPL + i];
+        V[i] += pp[D + lane * EPL + i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) K[i] *= scale;
+    store_row<T, EPL>(dk + col * (int64_t)(D * sizeof(T)), lane, K);
+    store_row<T, EPL>(dv + col * (int64_t)(D * sizeof(T)), lane, V);
+  }
+}
+
 template <typename K>
 int merge_grid(K, int64_t ids) {  // one warp per heavy row, at most 4 blocks per SM (tiny kernels)
   static int sms = 0;
@@ -184,6 +234,13 @@ MergeArgs merge_args(const ChunkTable& ht, const DevBuf& part, float scale) {
 
 template <typename T, int H, int D>
 struct Merges {
+  static gt_status run_list(int64_t nids, const int32_t* ids, const int64_t* ptr, const int64_t* idx,
+                            const float* part, char* dk, char* dv, float scale, cudaStream_t st) {
+    colb_merge_list_kernel<T, H, D><<<merge_grid(colb_merge_list_kernel<T, H, D>, nids), kBlock, 0, st>>>(
+        nids, ids, ptr, idx, part, dk, dv, scale);
+    GT_CUDA_TRY(cudaGetLastError());
+    return GT_OK;
+  }
   static gt_status run(int pass, const MergeArgs& m, cudaStream_t st) {
     if (pass == 0) fwd_merge_kernel<T, H, D><<<merge_grid(fwd_merge_kernel<T, H, D>, m.nids), kBlock, 0, st>>>(m);
     else if (pass == 1)
@@ -193,6 +250,21 @@ struct Merges {
     return GT_OK;
   }
 };
+
+gt_status merge_list(int dtype, int H, int D, int64_t nids, const int32_t* ids, const int64_t* ptr,
+                     const int64_t* idx, const float* part, char* dk, char* dv, float scale, cudaStream_t st) {
+#define GT_CASE(TT, HH, DD) \
+  if (H == HH && D == DD) return Merges<TT, HH, DD>::run_list(nids, ids, ptr, idx, part, dk, dv, scale, st);
+#define GT_HCASES(TT)                                                                              \
+  GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
+  GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
+  GT_CASE(TT, 8, 256) GT_CASE(TT, 8, 512)
+  if (dtype == GT_F32) { GT_HCASES(float) }
+  else { GT_HCASES(__nv_bfloat16) }
+#undef GT_HCASES
+#undef GT_CASE
+  return fail(GT_ECONFIG, "unsupported (dtype, heads, heads*d)");
+}
 
 gt_status merge(int dtype, int H, int D, int pass, const MergeArgs& m, cudaStream_t st) {
 #define GT_CASE(TT, HH, DD) \
@@ -224,6 +296,9 @@ int launches_fwd(const gt_plan_s* P) {
 }
 int launches_bwd(const gt_plan_s* P) {
   const int rows = (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
+  if (P->bwd_reduce)
+    return rows + (P->w_hcols.n > 0 ? 1 : 0) + (P->n_slots > 0 ? 1 : 0) + (P->w_colrs.n > 0 ? 1 : 0) +
+           (P->rs_chunks.ids.empty() ? 0 : 1);
   if (P->col_split)
     return rows + (P->w_colp[0].n > 0 ? 1 : 0) + (P->w_colp[1].n > 0 ? 1 : 0) + (P->col_chunks.nchunks() > 0 ? 1 : 0);
   return rows + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_cols.nchunks() > 0 ? 1 : 0);
@@ -311,6 +386,55 @@ gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void
     m.dv = (char*)dv;
     GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 2, m, st));
   }
+  return GT_OK;
+}
+
+// Reduce-scatter backward, sender side: the column pass over the halo columns (local rows' entries
+// with remote columns, grouped by slot; own k, v = the [k | v] rows received in the forward), every
+// piece a chunk partial, then summed per slot into the send rows.
+gt_status launch_bwd_halo_cols(gt_plan_s* P, const void* q, const void* dy, cudaStream_t st) {
+  const int elt = P->dtype == GT_F32 ? 4 : 2;
+  const int64_t RB = (int64_t)P->heads * P->d * elt;
+  if (P->w_hcols.n > 0) {
+    EntryState e;
+    if (P->es) {
+      e.in = P->d_pd.as<float>();
+      e.src = P->d_hsrc.as<int32_t>();
+    }
+    e.nbr = P->d_hrow.as<int32_t>();
+    e.nnbr = P->n_hent;
+    e.own_stride = 2 * RB;
+    const char* kv = (const char*)P->d_recv_kv.p;
+    GT_TRY(pipe_pass(P, 2, P->w_hcols, P->hcol_chunks, P->d_part_h.as<float>(), kv, kv + RB, nullptr, q, dy, nullptr,
+                     nullptr, nullptr, nullptr, nullptr, st, 0, e));
+  }
+  if (P->n_slots > 0) {
+    const int64_t row4 = 2 * (int64_t)P->heads * P->d / 4;
+    sum_slots_kernel<<<merge_grid(sum_slots_kernel, P->n_slots), kBlock, 0, st>>>(
+        P->n_slots, P->hcol_chunks.d_first.as<int32_t>(), (const float4*)P->d_part_h.p, row4, (float4*)P->d_rs_send.p);
+    GT_CUDA_TRY(cudaGetLastError());
+  }
+  return GT_OK;
+}
+
+// Reduce-scatter backward, owner side: owned columns over owned-row entries (columns with remote
+// in-edges leave chunk partials), then, once the partials of the peers are in (`recv_ready`), the
+// fixed-order merge of those columns.
+gt_status launch_bwd_cols_rs(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy, void* dk,
+                             void* dv, cudaStream_t st, cudaEvent_t recv_ready) {
+  EntryState e;
+  if (P->es) {
+    e.in = P->d_pd.as<float>();
+    e.src = P->d_src.as<int32_t>();
+  }
+  GT_TRY(pipe_pass(P, 2, P->w_colrs, P->rs_chunks, P->d_part_rs.as<float>(), k, v, nullptr, q, dy, nullptr, nullptr,
+                   dk, dv, nullptr, st, 0, e));
+  if (recv_ready) GT_CUDA_TRY(cudaStreamWaitEvent(st, recv_ready, 0));
+  const int64_t nids = (int64_t)P->rs_chunks.ids.size();
+  if (nids > 0)
+    GT_TRY(merge_list(P->dtype, P->heads, P->heads * P->d, nids, P->rs_chunks.d_ids.as<int32_t>(),
+                      P->d_mptr.as<int64_t>(), P->d_midx.as<int64_t>(), P->d_part_rs.as<float>(), (char*)dk,
+                      (char*)dv, P->scale, st));
   return GT_OK;
 }
 

@@ -145,6 +145,8 @@ struct PArgs {
   int64_t n_local;
   const char* oa;        // own tensor A (q | q | k)
   const char* ob;        // own tensor B (- | dy | v)
+  int64_t own_stride;    // bytes between own rows of the column pass (a feature row, or 2 of them when
+                         // the own rows are the [k | v] rows received in the forward)
   const float* lse;      // pass 1: caller's LSE [n_local][H] (natural log)
   char* out_a;           // y | dq | dk
   char* out_b;           // - | - | dv
@@ -513,8 +515,8 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
         cp_async<4>(o + C::OWN_LSE + head * 4, a.lse + r * H + head);
       } else if constexpr (!(ES & 1)) {
-        cp_slice<LB>(o, a.oa + r * RB, lane);
-        cp_slice<LB>(o + RB, a.ob + r * RB, lane);
+        cp_slice<LB>(o, a.oa + r * a.own_stride, lane);
+        cp_slice<LB>(o + RB, a.ob + r * a.own_stride, lane);
       }
       cur_first = false;
     }
@@ -793,8 +795,9 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.iown = w.d_own.as<int32_t>();
   a.nitems = w.n;
   a.cown = ct.d_owner.as<int32_t>();
-  a.nbr = (rows ? P->d_col : P->d_row).as<int32_t>();
-  a.nnbr = rows ? P->nnz_local : P->nnz_in_local;
+  a.nbr = es.nbr ? es.nbr : (rows ? P->d_col : P->d_row).as<int32_t>();
+  a.nnbr = es.nbr ? es.nnbr : (rows ? P->nnz_local : P->nnz_in_local);
+  a.own_stride = es.own_stride ? es.own_stride : (int64_t)P->heads * P->d * (P->dtype == GT_F32 ? 4 : 2);
   a.counter = w.d_counter.as<unsigned long long>();
   a.ga = (const char*)gather_a;
   a.gb = (const char*)gather_b;

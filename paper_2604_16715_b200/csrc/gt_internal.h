@@ -144,6 +144,25 @@ struct gt_plan_s {
   gt::WorkList w_colp[2];
   gt::ChunkTable col_chunks;
 
+  // paper-faithful backward (opts.bwd_mode = 1; "matching Reduce-Scatter", reading
+  // Z11): each rank computes fp32 partial dK || dV of the remote columns its rows touch ("halo
+  // columns", from the local CSR's remote-column entries grouped by slot), sends them to the owners
+  // (the forward pattern reversed: a reduce-scatter for all-gather, a reverse halo for halo), and
+  // each owner sums, in a fixed order, its local-row contributions and the received partials.
+  bool bwd_reduce = false;
+  gt::DevBuf d_hrow, d_hsrc;       // int32 [halo entries]: local row, local CSR entry; grouped by slot
+  int64_t n_hent = 0, n_slots = 0;
+  gt::WorkList w_hcols;            // one chunk item per <= T-entry piece of a halo column
+  gt::ChunkTable hcol_chunks;      // ids = every slot (possibly with no pieces)
+  gt::WorkList w_colrs;            // owned columns, owned-row entries; columns with remote in-edges merged
+  gt::ChunkTable rs_chunks;
+  gt::DevBuf d_part_h;             // f32 [halo pieces][2 D]
+  gt::DevBuf d_rs_send;            // f32 [slots][2 D]: summed partials, in slot (= owner-grouped) order
+  gt::DevBuf d_part_rs;            // f32 [rs chunks + received rows][2 D] (one index space)
+  gt::DevBuf d_mptr, d_midx;       // per merged column: rows of d_part_rs to sum, in a fixed order
+  std::vector<int64_t> rs_send_off, rs_send_cnt, rs_recv_off, rs_recv_cnt;
+  int64_t rs_recv_rows = 0, rs_row_bytes = 0;
+
   // multi-rank exchange
   gt::Comm* comm = nullptr;
   bool own_comm = true;
@@ -189,6 +208,11 @@ gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
                           const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st,
                           cudaEvent_t side_ready);
+// reduce-scatter backward: partials of the halo columns summed per slot into d_rs_send (st)
+gt_status launch_bwd_halo_cols(gt_plan_s* P, const void* q, const void* dy, cudaStream_t st);
+// reduce-scatter backward: owned columns from owned rows; merged columns completed after `recv_ready`
+gt_status launch_bwd_cols_rs(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy, void* dk,
+                             void* dv, cudaStream_t st, cudaEvent_t recv_ready);
 bool shape_supported(int heads, int d, int dtype);
 int launches_fwd(const gt_plan_s* P);
 int launches_bwd(const gt_plan_s* P);
@@ -197,7 +221,11 @@ int launches_bwd(const gt_plan_s* P);
 struct EntryState {
   float* out = nullptr;          // fwd: s2 [nnz_local][heads] | rowb: (P, dP) [nnz_local][heads][2]
   const float* in = nullptr;     // rowb: s2 | colb: (P, dP)
-  const int32_t* src = nullptr;  // colb: local CSC position -> local CSR entry (-1: remote row)
+  const int32_t* src = nullptr;  // colb: entry -> local CSR entry (-1: remote row)
+  // column pass over another entry list (the halo columns of the reduce-scatter backward)
+  const int32_t* nbr = nullptr;  // neighbour (row) ids of the entries; null: the plan's CSC slice
+  int64_t nnbr = 0;
+  int64_t own_stride = 0;        // bytes between own rows (0: one feature row)
 };
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
                     const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
@@ -232,6 +260,8 @@ std::vector<int32_t> send_set(int64_t n, const int64_t* row_ptr, const int32_t* 
 // segment longer than `threshold` is cut into equal chunks; a row with exactly one piece becomes a
 // whole-row item, otherwise every piece is a chunk of `t` (merged in entry order).  Rows without
 // entries become empty items in phase 0 (their outputs are written as empty rows).
+// force(r) (optional): r is always listed in the chunk table (all its pieces, possibly none, are chunks),
+// for outputs that are completed by a merge with contributions from elsewhere.
 void build_work(int64_t count, const std::function<void(int64_t, std::vector<Segment>&)>& segs, int64_t threshold,
-                int nphase, WorkList* phases, ChunkTable* t);
+                int nphase, WorkList* phases, ChunkTable* t, const std::function<bool(int64_t)>& force = nullptr);
 }  // namespace gt

@@ -136,7 +136,7 @@ std::vector<int32_t> send_set(int64_t n, const int64_t* rp, const int32_t* ci, i
 }
 
 void build_work(int64_t count, const std::function<void(int64_t, std::vector<Segment>&)>& segs, int64_t threshold,
-                int nphase, WorkList* phases, ChunkTable* t) {
+                int nphase, WorkList* phases, ChunkTable* t, const std::function<bool(int64_t)>& force) {
   t->ids.clear(); t->first.clear(); t->chunk_lo.clear(); t->chunk_hi.clear(); t->chunk_owner.clear();
   for (int ph = 0; ph < nphase; ++ph) {
     phases[ph].beg.clear(); phases[ph].end.clear(); phases[ph].own.clear();
@@ -153,7 +153,16 @@ void build_work(int64_t count, const std::function<void(int64_t, std::vector<Seg
       for (int64_t c = 0; c < nch; ++c)
         pieces.push_back({s.lo + len * c / nch, s.lo + len * (c + 1) / nch, s.phase});
     }
-    if (pieces.empty()) {
+    if (force && force(r)) {
+      t->ids.push_back((int32_t)r);
+      t->first.push_back((int32_t)t->chunk_lo.size());
+      for (const Segment& p : pieces) {
+        const int32_t ch = (int32_t)t->chunk_lo.size();
+        t->chunk_lo.push_back(p.lo); t->chunk_hi.push_back(p.hi); t->chunk_owner.push_back((int32_t)r);
+        WorkList& w = phases[p.phase];
+        w.beg.push_back(p.lo); w.end.push_back(p.hi); w.own.push_back(-1 - ch);
+      }
+    } else if (pieces.empty()) {
       const int64_t at = sg.empty() ? 0 : sg.front().lo;
       phases[0].beg.push_back(at); phases[0].end.push_back(at); phases[0].own.push_back((int32_t)r);
     } else if (pieces.size() == 1) {

@@ -18,7 +18,7 @@ from tests._util import TOL, check_lse, inputs, normwise, to_f64, to_torch
 pytestmark = pytest.mark.gpu
 
 
-def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0):
+def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0, bwd_mode=0):
     import torch
     import paper_2604_16715_b200 as gt
     n = len(rp) - 1
@@ -34,7 +34,8 @@ def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=
             torch.cuda.set_device(0)
             s = torch.cuda.Stream()
             plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, world=world, rank=r, comm=grp,
-                           strategy=strategy, heavy_threshold=heavy, partition=partition, edge_state=edge_state)
+                           strategy=strategy, heavy_threshold=heavy, partition=partition, edge_state=edge_state,
+                           bwd_mode=bwd_mode)
             lo, hi = plan.row_lo, plan.row_hi
             with torch.cuda.stream(s):
                 tq, tk, tv, tdy = (t[lo:hi].contiguous() for t in full)
@@ -89,31 +90,50 @@ def check(rp, ci, dtype, ins, res, world, partition=0):
         np.testing.assert_array_equal(ex["csc_idx"], ri[cp[lo]:cp[hi]])
 
 
+# bwd_mode 0: transposed owner (default); 1: reduce-scatter of fp32 partials (paper-faithful, Z11)
+@pytest.mark.parametrize("bwd_mode", [0, 1])
 @pytest.mark.parametrize("edge_state", [1, -1])
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("strategy", ["halo", "allgather"])
-def test_loopback_directed_power_law(world, strategy, edge_state):
+def test_loopback_directed_power_law(world, strategy, edge_state, bwd_mode):
     rp, ci = gtgen.random_graph(2500, 30000, seed=70 + world, directed=True, power=2.1)
     ins, res = run_loopback(rp, ci, 4, 64, "bf16", world, strategy, seed=700 + world, heavy=64,
-                            edge_state=edge_state)
+                            edge_state=edge_state, bwd_mode=bwd_mode)
     check(rp, ci, "bf16", ins, res, world)
     for r in res:
         assert r[4]["strategy_name"] == strategy
         assert r[4]["edge_state"] == (0 if edge_state < 0 else 1)
+        assert r[4]["bwd_mode"] == bwd_mode
 
 
-def test_loopback_communities_f32_auto():
+@pytest.mark.parametrize("bwd_mode", [0, 1])
+def test_loopback_communities_f32_auto(bwd_mode):
     rp, ci = gtgen.random_graph(4096, 50000, seed=81, directed=False, power=2.2, comm_size=512, f_in=0.9)
-    ins, res = run_loopback(rp, ci, 8, 16, "f32", 4, "auto", seed=801)
+    ins, res = run_loopback(rp, ci, 8, 16, "f32", 4, "auto", seed=801, bwd_mode=bwd_mode)
     check(rp, ci, "f32", ins, res, 4)
     chosen = {r[4]["strategy_name"] for r in res}
     assert len(chosen) == 1 and chosen <= {"halo", "allgather"}  # every rank applies rank 0's decision
 
 
-def test_loopback_more_ranks_than_rows_and_node_partition():
+@pytest.mark.parametrize("bwd_mode", [0, 1])
+def test_loopback_more_ranks_than_rows_and_node_partition(bwd_mode):
     rp, ci = gtgen.csr_from_pairs(3, [(0, 1), (1, 2), (2, 0), (2, 1)])
-    ins, res = run_loopback(rp, ci, 2, 64, "f32", 5, "halo", seed=901)
+    ins, res = run_loopback(rp, ci, 2, 64, "f32", 5, "halo", seed=901, bwd_mode=bwd_mode)
     check(rp, ci, "f32", ins, res, 5)
     rp, ci = gtgen.random_graph(700, 6000, seed=91, power=2.3)
-    ins, res = run_loopback(rp, ci, 4, 32, "bf16", 3, "allgather", seed=902, partition=1)
+    ins, res = run_loopback(rp, ci, 4, 32, "bf16", 3, "allgather", seed=902, partition=1, bwd_mode=bwd_mode)
     check(rp, ci, "bf16", ins, res, 3, partition=1)
+
+
+def test_reduce_scatter_hub_columns_chunked_and_deterministic():
+    """Hub columns with more in-edges than the chunk threshold on several ranks: partial pieces, a
+    summed send row per slot and a multi-source merge; two runs are bitwise identical."""
+    n = 900
+    pairs = [(i, 0) for i in range(1, n)] + [(i, n - 1) for i in range(0, n - 1)] + [(0, j) for j in range(1, n)]
+    rp, ci = gtgen.csr_from_pairs(n, pairs)
+    outs = []
+    for _ in range(2):
+        ins, res = run_loopback(rp, ci, 4, 64, "f32", 3, "halo", seed=911, heavy=50, bwd_mode=1)
+        check(rp, ci, "f32", ins, res, 3)
+        outs.append(np.concatenate([np.concatenate([r[2][i] for r in res]).ravel() for i in (0, 2, 3, 4)]))
+    assert np.array_equal(outs[0], outs[1])
