@@ -70,7 +70,11 @@ typedef enum {
   GT_AUTO = 0,      /* cost-model choice (world > 1); GT_SINGLE when world == 1 */
   GT_SINGLE = 1,    /* world == 1 only */
   GT_ALLGATHER = 2, /* GP-AG: every rank receives every remote K||V row (Alg. 1) */
-  GT_HALO = 3       /* only the rows its cut edges touch (reading of Alg. 3's open set) */
+  GT_HALO = 3,      /* only the rows its cut edges touch (reading of Alg. 3's open set) */
+  GT_A2A = 4        /* GP-A2A head parallelism (Alg. 2): all-to-all of Q, K, V by head group,
+                       every rank runs all N rows for heads / world heads, all-to-all of Y back.  Needs
+                       heads % world == 0 and a supported (heads / world, d) shape; Q, K, V (and LSE)
+                       head slices are retained from gt_attn_fwd for gt_attn_bwd. */
 } gt_strategy;
 
 typedef enum {
@@ -132,10 +136,10 @@ typedef struct {
   int64_t device_bytes;           /* device memory held by the plan */
   int64_t heavy_rows, heavy_row_chunks, heavy_cols, heavy_col_chunks;
   int launches_fwd, launches_bwd; /* libgt kernels launched per call */
-  double beta_s_per_row[4];       /* measured exchange time per received row, by strategy (s) */
-  double predicted_ms[4];         /* cost-model time of fwd+bwd, by strategy (ms) */
-  double agp_score[4];            /* Alg. 3 score p * t_comm / (p - 1) per strategy (ms) */
-  int agp_feasible[4];            /* Eq. 14 feasibility: score <= t_iter(1) */
+  double beta_s_per_row[5];       /* measured exchange time per received row, by strategy (s) */
+  double predicted_ms[5];         /* cost-model time of fwd+bwd, by strategy (ms) */
+  double agp_score[5];            /* Alg. 3 score p * t_comm / (p - 1) per strategy (ms) */
+  int agp_feasible[5];            /* Eq. 14 feasibility: score <= t_iter(1) */
   double alpha_s_per_unit;        /* cost-model compute seconds per (edge + row) */
   int edge_state;                 /* 1 if the plan materialises per-entry state (gt_opts.edge_state) */
   int64_t edge_state_bytes;       /* device bytes of that state */

@@ -206,6 +206,7 @@ gt_plan_s::~gt_plan_s() {
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
   if (comm && own_comm) delete comm;
+  delete sub;
 }
 
 static bool ag_of(const gt_plan_s* P) { return P->strategy == GT_ALLGATHER; }
@@ -304,6 +305,98 @@ static gt_status build_reduce_backward(gt_plan_s* P, const gt_csr* csr, const st
 }
 
 extern "C" {
+static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads, int d, int world,
+                           const gt_opts* opts, gt_plan_t* out);
+}
+
+static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
+  const bool single = P->world == 1;
+  gt_plan_info& I = P->info;
+  I.world = P->world; I.rank = P->rank; I.strategy = P->strategy; I.dtype = P->dtype; I.heads = P->heads;
+  I.d = P->d; I.scale = P->scale; I.n = P->n; I.nnz = P->nnz; I.row_lo = P->lo; I.row_hi = P->hi;
+  I.n_local = P->n_local; I.nnz_local = P->nnz_local; I.nnz_in_local = P->nnz_in_local;
+  I.halo_out_rows = single ? 0 : (P->strategy == GT_ALLGATHER ? (int64_t)(P->world - 1) * P->n_max : (int64_t)P->halo_out.size());
+  I.halo_in_rows = single ? 0 : (P->strategy == GT_ALLGATHER ? (int64_t)(P->world - 1) * P->n_max : (int64_t)P->halo_in.size());
+  I.heavy_rows = (int64_t)P->heavy_rows.ids.size();
+  I.heavy_row_chunks = nrc;
+  I.heavy_cols = (int64_t)P->heavy_cols.ids.size();
+  I.heavy_col_chunks = ncc;
+  I.launches_fwd = launches_fwd(P) + (single ? 0 : 1);
+  I.launches_bwd = launches_bwd(P) + (single ? 0 : (P->bwd_reduce ? 0 : 1));
+  I.bwd_mode = P->bwd_reduce ? 1 : 0;
+  int64_t dev = 0;
+  for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
+                          &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
+                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src,
+                          &P->d_hrow, &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx,
+                          &P->d_hq, &P->d_hk, &P->d_hv, &P->d_hy, &P->d_hlse, &P->d_hdy, &P->d_hdq, &P->d_hdk,
+                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2]})
+    dev += (int64_t)b->bytes;
+  if (P->strategy == GT_A2A && P->sub) {  // the world-1 plan over all rows with heads / world heads
+    const gt_plan_info& S = P->sub->info;
+    dev += S.device_bytes;
+    I.heavy_rows = S.heavy_rows; I.heavy_row_chunks = S.heavy_row_chunks;
+    I.heavy_cols = S.heavy_cols; I.heavy_col_chunks = S.heavy_col_chunks;
+    I.launches_fwd = S.launches_fwd + 5;   // 3 packs + 2 unpacks (Y, LSE)
+    I.launches_bwd = S.launches_bwd + 5;   // 2 packs (dY, LSE) + 3 unpacks
+    I.edge_state = S.edge_state; I.edge_state_bytes = S.edge_state_bytes;
+    const int64_t gb = (int64_t)P->heads_l * P->d * (P->dtype == GT_F32 ? 4 : 2);
+    const int64_t remote = P->n - P->n_local;
+    I.exch_fwd_bytes = remote * (3 * gb + P->heads_l * 4) + (P->world - 1) * P->n_local * (gb + P->heads_l * 4);
+    I.exch_bwd_bytes = remote * (gb + P->heads_l * 4) + (P->world - 1) * P->n_local * 3 * gb;
+  }
+  I.device_bytes = dev;
+}
+
+// GP-A2A: the world-1 plan over the full graph with heads / world heads, head-slice buffers and the
+// two all-to-all patterns (rows in head-group units: local block -> all rows of the rank's heads).
+static gt_status build_a2a(gt_plan_s* P, const gt_csr* csr, int64_t n, int64_t nnz, int d, const gt_opts* opts) {
+  const int w = P->world;
+  P->heads_l = P->heads / w;
+  gt_opts so = *opts;
+  so.rank = 0;
+  so.comm_kind = GT_COMM_NONE;
+  so.comm = nullptr;
+  so.strategy = GT_SINGLE;
+  so.bwd_mode = 0;
+  so.validate = 0;  // validated by the caller
+  so.device = P->device;
+  so.scale = P->scale;  // 1 / sqrt(heads d) of the full problem, not of the head slice
+  gt_plan_t sub = nullptr;
+  GT_TRY(plan_impl(csr, n, nnz, P->heads_l, d, 1, &so, &sub));
+  P->sub = sub;
+  const int elt = P->dtype == GT_F32 ? 4 : 2;
+  const int64_t gb = (int64_t)P->heads_l * d * elt;
+  const size_t nn = (size_t)std::max<int64_t>(n, 1);
+  for (DevBuf* b : {&P->d_hq, &P->d_hk, &P->d_hv, &P->d_hy, &P->d_hdy, &P->d_hdq, &P->d_hdk, &P->d_hdv})
+    GT_TRY(b->alloc(nn * gb));
+  GT_TRY(P->d_hlse.alloc(nn * P->heads_l * sizeof(float)));
+  for (DevBuf& b : P->d_stage)
+    GT_TRY(b.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->heads * d * elt));
+  P->a2a_loc_off.resize(w); P->a2a_loc_cnt.resize(w); P->a2a_glob_off.resize(w); P->a2a_glob_cnt.resize(w);
+  for (int s = 0; s < w; ++s) {
+    P->a2a_loc_off[s] = (int64_t)s * P->n_local;
+    P->a2a_loc_cnt[s] = s == P->rank ? 0 : P->n_local;
+    P->a2a_glob_off[s] = P->bounds[s];
+    P->a2a_glob_cnt[s] = s == P->rank ? 0 : P->bounds[s + 1] - P->bounds[s];
+  }
+  return GT_OK;
+}
+
+// Scatter of a row-partitioned tensor [n_local][heads groups of gb bytes] into the head slice
+// [n][gb] of this rank (stage: [world][n_local][gb]); gather is the reverse.
+static gt_status a2a_scatter(gt_plan_s* P, const void* src, int64_t gb, void* stage, void* slice, cudaStream_t st) {
+  GT_TRY(a2a_pack(src, P->n_local, P->world, gb, P->rank, stage, (char*)slice + P->lo * gb, st));
+  return P->comm->exchange(stage, P->a2a_loc_off.data(), P->a2a_loc_cnt.data(), slice, P->a2a_glob_off.data(),
+                           P->a2a_glob_cnt.data(), gb, st);
+}
+static gt_status a2a_gather(gt_plan_s* P, const void* slice, int64_t gb, void* stage, void* dst, cudaStream_t st) {
+  GT_TRY(P->comm->exchange(slice, P->a2a_glob_off.data(), P->a2a_glob_cnt.data(), stage, P->a2a_loc_off.data(),
+                           P->a2a_loc_cnt.data(), gb, st));
+  return a2a_unpack(stage, (const char*)slice + P->lo * gb, P->n_local, P->world, gb, P->rank, dst, st);
+}
+
+extern "C" {
 
 const char* gt_last_error(void) { return g_err.c_str(); }
 
@@ -334,8 +427,11 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   if (world < 1 || opts->rank < 0 || opts->rank >= world) return fail(GT_EINVAL, "gt_plan: bad world/rank");
   if (world > 1 && (!opts->comm || (opts->comm_kind != GT_COMM_NCCL && opts->comm_kind != GT_COMM_LOOPBACK)))
     return fail(GT_EINVAL, "gt_plan: world > 1 needs a communicator");
-  if (world == 1 && (opts->strategy == GT_ALLGATHER || opts->strategy == GT_HALO))
+  if (opts->strategy < GT_AUTO || opts->strategy > GT_A2A) return fail(GT_EINVAL, "gt_plan: unknown strategy");
+  if (world == 1 && (opts->strategy == GT_ALLGATHER || opts->strategy == GT_HALO || opts->strategy == GT_A2A))
     return fail(GT_ECONFIG, "gt_plan: multi-GPU strategy requested with world == 1");
+  if (world > 1 && opts->strategy == GT_A2A && (heads % world != 0 || !shape_supported(heads / world, d, opts->dtype)))
+    return fail(GT_ECONFIG, "gt_plan: GP-A2A needs heads % world == 0 and a supported (heads / world, d) shape");
   if (opts->partition != 0 && opts->partition != 1) return fail(GT_EINVAL, "gt_plan: partition must be 0 or 1");
   if (opts->bwd_mode != 0 && opts->bwd_mode != 1) return fail(GT_EINVAL, "gt_plan: bwd_mode must be 0 or 1");
   if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
@@ -405,6 +501,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   // ---- local column slice (column pass) ----
   const int64_t c0 = col_ptr_full[P->lo], c1 = col_ptr_full[P->hi];
   P->nnz_in_local = c1 - c0;
+  P->csc_base = c0;
   P->h_col_ptr.resize((size_t)P->n_local + 1);
   for (int64_t j = 0; j <= P->n_local; ++j) P->h_col_ptr[j] = col_ptr_full[P->lo + j] - c0;
 
@@ -499,14 +596,72 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       if (!fits && strategy == c) return fail(GT_ENOMEM, "gt_plan: strategy buffers do not fit in device memory");
     }
     P->info.predicted_ms[GT_SINGLE] = t_iter1 * 1e3;
+    // GP-A2A (Alg. 2; Table 1 volume 8 N d / p): every rank does heads / world of all
+    // the work; 4 all-to-alls of head groups per direction (Q, K, V in + Y out; dY in + dQ, dK, dV out)
+    P->info.predicted_ms[GT_A2A] = INFINITY;
+    P->info.agp_score[GT_A2A] = INFINITY;
+    if (heads % world == 0 && shape_supported(heads / world, d, opts->dtype) &&
+        (strategy == GT_AUTO || strategy == GT_A2A)) {
+      const int64_t gb = (int64_t)(heads / world) * d * elt;
+      const int64_t sub_bytes = nnz * (12 + (int64_t)(heads / world) * 12) + n * 40;   // graph + entry state
+      const int64_t need = 9 * n * gb + 3 * P->n_max * D * elt + sub_bytes;
+      size_t free_a = 0, total_a = 0;
+      GT_CUDA_TRY(cudaMemGetInfo(&free_a, &total_a));
+      double misfit = (double)need < 0.85 * (double)free_a ? 0.0 : 1.0;
+      GT_TRY(P->comm->max_host(&misfit, st));
+      if (misfit > 0 && strategy == GT_A2A) return fail(GT_ENOMEM, "gt_plan: GP-A2A buffers do not fit in device memory");
+      if (misfit == 0 && strategy == GT_AUTO) {
+        std::vector<int64_t> loff(world), lcnt(world), goff(world), gcnt(world);
+        for (int s = 0; s < world; ++s) {
+          loff[s] = (int64_t)s * P->n_local;
+          lcnt[s] = s == P->rank ? 0 : P->n_local;
+          goff[s] = P->bounds[s];
+          gcnt[s] = s == P->rank ? 0 : P->bounds[s + 1] - P->bounds[s];
+        }
+        DevBuf sb, rb;
+        GT_TRY(sb.alloc((size_t)std::max<int64_t>(world * P->n_local * gb, 16)));
+        GT_TRY(rb.alloc((size_t)std::max<int64_t>(n * gb, 16)));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float ms_best = 1e30f;
+        for (int it = 0; it < 5; ++it) {
+          GT_TRY(P->comm->barrier(st));
+          cudaEventRecord(e0, st);
+          for (int x = 0; x < 8; ++x)
+            GT_TRY(P->comm->exchange(sb.p, loff.data(), lcnt.data(), rb.p, goff.data(), gcnt.data(), gb, st));
+          cudaEventRecord(e1, st);
+          GT_CUDA_TRY(cudaEventSynchronize(e1));
+          float ms = 0;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (it >= 2) ms_best = std::min(ms_best, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        double t_ex = ms_best * 1e-3;
+        GT_TRY(P->comm->max_host(&t_ex, st));
+        const double rows = 8.0 * (double)(n - P->n_local);
+        P->info.beta_s_per_row[GT_A2A] = rows > 0 ? t_ex / rows : 0.0;
+        P->info.predicted_ms[GT_A2A] = (t_iter1 / world + t_ex) * 1e3;
+        P->info.agp_score[GT_A2A] = world * t_ex / (world - 1) * 1e3;
+        P->info.agp_feasible[GT_A2A] = world * t_ex / (world - 1) <= t_iter1;
+      }
+    }
     if (strategy == GT_AUTO) {
       int32_t pick = P->info.predicted_ms[GT_HALO] < P->info.predicted_ms[GT_ALLGATHER] ? GT_HALO : GT_ALLGATHER;
+      if (P->info.predicted_ms[GT_A2A] < P->info.predicted_ms[pick]) pick = GT_A2A;
       GT_TRY(P->comm->broadcast_host(&pick, sizeof(pick), st));  // rank 0 decides
       strategy = pick;
     }
     P->strategy = strategy;
   } else {
     P->strategy = GT_SINGLE;
+  }
+  if (P->strategy == GT_A2A) {
+    GT_TRY(build_a2a(P.get(), csr, n, nnz, d, opts));
+    fill_info(P.get(), 0, 0);
+    *out = P.release();
+    return GT_OK;
   }
 
   // ---- remapped local CSR columns and CSC rows ----
@@ -662,27 +817,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->stats_stride * sizeof(float)));
   GT_CUDA_TRY(cudaStreamSynchronize(st));
 
-  // ---- info ----
-  gt_plan_info& I = P->info;
-  I.world = world; I.rank = P->rank; I.strategy = P->strategy; I.dtype = P->dtype; I.heads = heads; I.d = d;
-  I.scale = P->scale; I.n = n; I.nnz = nnz; I.row_lo = P->lo; I.row_hi = P->hi; I.n_local = P->n_local;
-  I.nnz_local = P->nnz_local; I.nnz_in_local = P->nnz_in_local;
-  I.halo_out_rows = single ? 0 : (P->strategy == GT_ALLGATHER ? (int64_t)(world - 1) * P->n_max : (int64_t)P->halo_out.size());
-  I.halo_in_rows = single ? 0 : (P->strategy == GT_ALLGATHER ? (int64_t)(world - 1) * P->n_max : (int64_t)P->halo_in.size());
-  I.heavy_rows = (int64_t)P->heavy_rows.ids.size();
-  I.heavy_row_chunks = nrc;
-  I.heavy_cols = (int64_t)P->heavy_cols.ids.size();
-  I.heavy_col_chunks = ncc;
-  I.launches_fwd = launches_fwd(P.get()) + (single ? 0 : 1);
-  I.launches_bwd = launches_bwd(P.get()) + (single ? 0 : (P->bwd_reduce ? 0 : 1));
-  I.bwd_mode = P->bwd_reduce ? 1 : 0;
-  int64_t dev = 0;
-  for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
-                          &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
-                          &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src, &P->d_hrow,
-                          &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx})
-    dev += (int64_t)b->bytes;
-  I.device_bytes = dev;
+  fill_info(P.get(), nrc, ncc);
   *out = P.release();
   return GT_OK;
 }
@@ -732,11 +867,13 @@ gt_status gt_plan_export(gt_plan_t P, int what, int peer, void* dst, int64_t cap
     case GT_EXPORT_CSC_IDX: {
       count = P->nnz_in_local;
       tmp32.resize((size_t)count);
+      // GP-A2A keeps the CSC only in its full-graph plan (global row ids): the owned-column slice
+      const int32_t* rows = P->sub ? P->sub->d_row.as<int32_t>() + P->csc_base : P->d_row.as<int32_t>();
       if (count) {
-        cudaError_t e = cudaMemcpy(tmp32.data(), P->d_row.p, (size_t)count * 4, cudaMemcpyDeviceToHost);
+        cudaError_t e = cudaMemcpy(tmp32.data(), rows, (size_t)count * 4, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return fail(GT_ECUDA, cudaGetErrorString(e));
       }
-      if (P->world > 1) {  // undo the remap: report global row ids
+      if (P->world > 1 && !P->sub) {  // undo the remap: report global row ids
         for (auto& x : tmp32) {
           int64_t i = x;
           if (i < P->n_local) x = (int32_t)(i + P->lo);
@@ -777,6 +914,23 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   GT_TRY(check_ptrs(P, {q, k, v, y, lse}));
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
+  if (P->strategy == GT_A2A) {  // GP-A2A (Alg. 2): scatter Q, K, V by head group, all rows, gather Y, LSE
+    const int64_t gb = (int64_t)P->heads_l * P->d * (P->dtype == GT_F32 ? 4 : 2);
+    const int64_t lb = (int64_t)P->heads_l * 4;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    P->mark_begin(0, st, &e0);
+    GT_TRY(a2a_scatter(P, q, gb, P->d_stage[0].p, P->d_hq.p, st));
+    GT_TRY(a2a_scatter(P, k, gb, P->d_stage[1].p, P->d_hk.p, st));
+    GT_TRY(a2a_scatter(P, v, gb, P->d_stage[2].p, P->d_hv.p, st));
+    P->mark_end(0, st, e0);
+    GT_TRY(gt_attn_fwd(P->sub, P->d_hq.p, P->d_hk.p, P->d_hv.p, P->d_hy.p, P->d_hlse.as<float>(), stream));
+    P->mark_begin(0, st, &e1);
+    GT_TRY(a2a_gather(P, P->d_hy.p, gb, P->d_stage[0].p, y, st));
+    GT_TRY(a2a_gather(P, P->d_hlse.p, lb, P->d_stage[1].p, lse, st));
+    P->mark_end(0, st, e1);
+    P->fwd_done = true;
+    return GT_OK;
+  }
   const void* halo = nullptr;
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   if (P->world > 1) {
@@ -809,6 +963,23 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   if (P->world > 1 && !P->fwd_done) return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd (halo K||V not retained)");
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
+  if (P->strategy == GT_A2A) {  // GP-A2A: scatter dY and LSE, all rows for this rank's heads, gather grads
+    const int64_t gb = (int64_t)P->heads_l * P->d * (P->dtype == GT_F32 ? 4 : 2);
+    const int64_t lb = (int64_t)P->heads_l * 4;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    P->mark_begin(3, st, &e0);
+    GT_TRY(a2a_scatter(P, dy, gb, P->d_stage[0].p, P->d_hdy.p, st));
+    GT_TRY(a2a_scatter(P, lse, lb, P->d_stage[1].p, P->d_hlse.p, st));
+    P->mark_end(3, st, e0);
+    GT_TRY(gt_attn_bwd(P->sub, P->d_hq.p, P->d_hk.p, P->d_hv.p, P->d_hlse.as<float>(), P->d_hdy.p, P->d_hdq.p,
+                       P->d_hdk.p, P->d_hdv.p, stream));
+    P->mark_begin(3, st, &e1);
+    GT_TRY(a2a_gather(P, P->d_hdq.p, gb, P->d_stage[0].p, dq, st));
+    GT_TRY(a2a_gather(P, P->d_hdk.p, gb, P->d_stage[1].p, dk, st));
+    GT_TRY(a2a_gather(P, P->d_hdv.p, gb, P->d_stage[2].p, dv, st));
+    P->mark_end(3, st, e1);
+    return GT_OK;
+  }
   const void* halo_kv = P->world > 1 ? P->d_recv_kv.p : nullptr;
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   const bool multi = P->world > 1;
@@ -919,6 +1090,15 @@ gt_status gt_plan_timings(gt_plan_t P, double* ms, int64_t* calls) {
     P->ev_pool.push_back(r.b);
   }
   P->recs.clear();
+  if (P->sub) {  // GP-A2A: the head-slice plan's stages
+    double sm[5];
+    int64_t sc[5];
+    GT_TRY(gt_plan_timings(P->sub, sm, sc));
+    for (int i = 0; i < 5; ++i) {
+      ms[i] += sm[i];
+      if (calls) calls[i] += sc[i];
+    }
+  }
   return GT_OK;
 }
 

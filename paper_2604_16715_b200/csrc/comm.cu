@@ -44,7 +44,66 @@ __global__ void pack_stats_kernel(const uint4* stats, const int32_t* idx, int64_
   }
 }
 
+// GP-A2A head-group transposes.  A row of `groups` head groups of `gb` bytes each:
+//   pack:   src[row][s] -> dst[s][row] (groups s != self), dst_self[row] (s == self)
+//   unpack: src[s][row] (s != self), src_self[row] (s == self) -> dst[row][s]
+template <typename U>
+__global__ void a2a_pack_kernel(const U* src, int64_t rows, int groups, int64_t gu, int self, U* dst, U* dst_self) {
+  const int64_t total = rows * groups * gu;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t % gu;
+    const int64_t rs = t / gu;
+    const int s = (int)(rs % groups);
+    const int64_t r = rs / groups;
+    const U x = src[t];
+    if (s == self) dst_self[r * gu + c] = x;
+    else dst[((int64_t)s * rows + r) * gu + c] = x;
+  }
+}
+template <typename U>
+__global__ void a2a_unpack_kernel(const U* src, const U* src_self, int64_t rows, int groups, int64_t gu, int self,
+                                  U* dst) {
+  const int64_t total = rows * groups * gu;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t % gu;
+    const int64_t rs = t / gu;
+    const int s = (int)(rs % groups);
+    const int64_t r = rs / groups;
+    dst[t] = s == self ? src_self[r * gu + c] : src[((int64_t)s * rows + r) * gu + c];
+  }
+}
+
 }  // namespace
+
+gt_status a2a_pack(const void* src, int64_t rows, int groups, int64_t gb, int self, void* dst, void* dst_self,
+                   cudaStream_t st) {
+  if (rows <= 0) return GT_OK;
+  const int64_t n = rows * groups * (gb % 16 == 0 ? gb / 16 : gb / 4);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (gb % 16 == 0)
+    a2a_pack_kernel<uint4><<<blocks, 256, 0, st>>>((const uint4*)src, rows, groups, gb / 16, self, (uint4*)dst,
+                                                   (uint4*)dst_self);
+  else
+    a2a_pack_kernel<uint32_t><<<blocks, 256, 0, st>>>((const uint32_t*)src, rows, groups, gb / 4, self,
+                                                      (uint32_t*)dst, (uint32_t*)dst_self);
+  GT_CUDA_TRY(cudaGetLastError());
+  return GT_OK;
+}
+
+gt_status a2a_unpack(const void* src, const void* src_self, int64_t rows, int groups, int64_t gb, int self, void* dst,
+                     cudaStream_t st) {
+  if (rows <= 0) return GT_OK;
+  const int64_t n = rows * groups * (gb % 16 == 0 ? gb / 16 : gb / 4);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (gb % 16 == 0)
+    a2a_unpack_kernel<uint4><<<blocks, 256, 0, st>>>((const uint4*)src, (const uint4*)src_self, rows, groups, gb / 16,
+                                                     self, (uint4*)dst);
+  else
+    a2a_unpack_kernel<uint32_t><<<blocks, 256, 0, st>>>((const uint32_t*)src, (const uint32_t*)src_self, rows, groups,
+                                                        gb / 4, self, (uint32_t*)dst);
+  GT_CUDA_TRY(cudaGetLastError());
+  return GT_OK;
+}
 
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt, void* out,
                   cudaStream_t st) {

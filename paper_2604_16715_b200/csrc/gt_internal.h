@@ -182,6 +182,17 @@ struct gt_plan_s {
   cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr, ev_fwd0 = nullptr, ev_halo = nullptr;
   bool fwd_done = false;
 
+  // GP-A2A head-parallel strategy (Alg. 2): a world-1 plan over
+  // the full graph with heads / world heads; Q, K, V, dY, LSE are scattered by head group (all-to-all,
+  // rows of this rank -> all rows of this rank's heads), Y, LSE, dQ, dK, dV gathered back.  The head
+  // slices of Q, K, V and LSE are retained from gt_attn_fwd for gt_attn_bwd.
+  gt_plan_s* sub = nullptr;
+  int heads_l = 0;
+  int64_t csc_base = 0;            // first entry of the owned columns in the global CSC
+  gt::DevBuf d_hq, d_hk, d_hv, d_hy, d_hlse, d_hdy, d_hdq, d_hdk, d_hdv;   // [n, heads_l, d] ([n, heads_l])
+  gt::DevBuf d_stage[3];                                                  // [world][n_local] head-group rows
+  std::vector<int64_t> a2a_loc_off, a2a_loc_cnt, a2a_glob_off, a2a_glob_cnt;  // per peer, in rows
+
   // end-to-end host staging
   gt::DevBuf h2d[9];
 
@@ -236,6 +247,12 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,
                   void* out, cudaStream_t st);
 gt_status pack_stats(const float* stats, const int32_t* idx, int64_t rows, int64_t row_bytes, void* out,
+                     cudaStream_t st);
+
+// GP-A2A head-group transposes (comm.cu); gb = bytes of one head group of a row
+gt_status a2a_pack(const void* src, int64_t rows, int groups, int64_t gb, int self, void* dst, void* dst_self,
+                   cudaStream_t st);
+gt_status a2a_unpack(const void* src, const void* src_self, int64_t rows, int groups, int64_t gb, int self, void* dst,
                      cudaStream_t st);
 
 // graph (graph.cu)

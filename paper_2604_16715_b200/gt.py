@@ -17,7 +17,7 @@ GT_OK, GT_EINVAL, GT_EGRAPH, GT_ECONFIG, GT_ENOMEM, GT_ECUDA, GT_ENCCL, GT_ESTAT
 STATUS_NAMES = ["GT_OK", "GT_EINVAL", "GT_EGRAPH", "GT_ECONFIG", "GT_ENOMEM", "GT_ECUDA", "GT_ENCCL", "GT_ESTATE"]
 GT_F32, GT_BF16 = 0, 1
 GT_AUTO, GT_SINGLE, GT_ALLGATHER, GT_HALO = range(4)
-STRATEGIES = {"auto": GT_AUTO, "single": GT_SINGLE, "allgather": GT_ALLGATHER, "halo": GT_HALO}
+STRATEGIES = {"auto": GT_AUTO, "single": GT_SINGLE, "allgather": GT_ALLGATHER, "halo": GT_HALO, "a2a": 4}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 GT_COMM_NONE, GT_COMM_NCCL, GT_COMM_LOOPBACK = range(3)
 EXPORT = {"bounds": 0, "halo_out": 1, "halo_in": 2, "send_out": 3, "send_in": 4, "csc_ptr": 5, "csc_idx": 6,
@@ -51,8 +51,8 @@ class _Info(ctypes.Structure):
                     "halo_in_rows", "exch_fwd_bytes", "exch_bwd_bytes", "send_fwd_bytes", "send_bwd_bytes",
                     "device_bytes", "heavy_rows", "heavy_row_chunks", "heavy_cols", "heavy_col_chunks")]
                 + [("launches_fwd", ctypes.c_int), ("launches_bwd", ctypes.c_int)]
-                + [("beta_s_per_row", ctypes.c_double * 4), ("predicted_ms", ctypes.c_double * 4),
-                   ("agp_score", ctypes.c_double * 4), ("agp_feasible", ctypes.c_int * 4),
+                + [("beta_s_per_row", ctypes.c_double * 5), ("predicted_ms", ctypes.c_double * 5),
+                   ("agp_score", ctypes.c_double * 5), ("agp_feasible", ctypes.c_int * 5),
                    ("alpha_s_per_unit", ctypes.c_double), ("edge_state", ctypes.c_int),
                    ("edge_state_bytes", ctypes.c_int64), ("bwd_mode", ctypes.c_int)])
 

@@ -137,3 +137,36 @@ def test_reduce_scatter_hub_columns_chunked_and_deterministic():
         check(rp, ci, "f32", ins, res, 3)
         outs.append(np.concatenate([np.concatenate([r[2][i] for r in res]).ravel() for i in (0, 2, 3, 4)]))
     assert np.array_equal(outs[0], outs[1])
+
+
+# GP-A2A head parallelism (Alg. 2): heads / world heads of all rows per rank
+@pytest.mark.parametrize("world,h,d,dtype", [(2, 4, 64, "bf16"), (2, 8, 32, "f32"), (4, 8, 64, "f32"),
+                                             (4, 8, 64, "bf16")])
+@pytest.mark.parametrize("edge_state", [1, -1])
+def test_loopback_a2a_head_parallel(world, h, d, dtype, edge_state):
+    rp, ci = gtgen.random_graph(2200, 28000, seed=120 + world + h, directed=True, power=2.1)
+    ins, res = run_loopback(rp, ci, h, d, dtype, world, "a2a", seed=1200 + world, heavy=64, edge_state=edge_state)
+    check(rp, ci, dtype, ins, res, world)
+    for r in res:
+        assert r[4]["strategy_name"] == "a2a"
+
+
+def test_a2a_infeasible_shapes_are_config_errors():
+    import paper_2604_16715_b200 as gt
+    rp, ci = gtgen.random_graph(300, 2000, seed=5, power=2.3)
+    grp = gt.LoopbackGroup(2)
+    try:
+        with pytest.raises(gt.GTError) as e:  # heads % world != 0 (checked before any collective)
+            gt.Plan(rp, ci, 1, 128, dtype="f32", world=2, rank=0, comm=grp, strategy="a2a")
+        assert e.value.status == 3
+    finally:
+        grp.close()
+
+
+def test_loopback_auto_considers_a2a():
+    rp, ci = gtgen.random_graph(3000, 40000, seed=131, directed=False, power=2.2)
+    ins, res = run_loopback(rp, ci, 8, 32, "bf16", 2, "auto", seed=1310)
+    check(rp, ci, "bf16", ins, res, 2)
+    for r in res:
+        assert np.isfinite(r[4]["predicted_ms"][4])  # GP-A2A probed and costed
+    assert len({r[4]["strategy_name"] for r in res}) == 1
