@@ -117,6 +117,37 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def report_fields(per_step, stages, info, world, nnz, step_bytes, peak):
+    """SURVEY.md 8(d) report: step-time spread, HBM fractions at the measured and the 8 TB/s peak,
+    exchanged bytes and their NVLink fraction (900 GB/s per direction), and the environment."""
+    import statistics
+    import torch
+    mean = statistics.fmean(per_step)
+    exch_ms = stages.get("fwd_exchange", (0.0, 0))[0] + stages.get("bwd_exchange", (0.0, 0))[0]
+    nsteps = max(len(per_step), 1)
+    exch_bytes = info["exch_fwd_bytes"] + info["exch_bwd_bytes"]
+    t_exch = exch_ms / nsteps
+    out = {
+        "t_ms_mean": mean, "t_ms_min": min(per_step), "t_ms_std": statistics.pstdev(per_step),
+        "t_fwd_ms": stages["fwd"][0] / nsteps if "fwd" in stages else None,
+        "t_bwd_ms": (stages["bwd_rows"][0] + stages["bwd_cols"][0]) / nsteps,
+        "edges_per_s_per_gpu": nnz / (mean * 1e-3) / world,
+        "B_alg_bytes": step_bytes, "hbm_frac_measured_peak": step_bytes / (mean * 1e-3) / 1e9 / peak,
+        "hbm_frac_8000": step_bytes / (mean * 1e-3) / 8e12,
+        "exch_bytes_per_rank": exch_bytes, "t_exch_ms": t_exch,
+        "nvlink_frac": (exch_bytes / (t_exch * 1e-3) / 900e9) if t_exch > 0 else None,
+        "gpu_name": torch.cuda.get_device_name(), "torch_cuda": torch.version.cuda,
+        "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if world > 1 else None,
+        "strategy": info["strategy_name"], "predicted_ms": info["predicted_ms"],
+    }
+    try:
+        out["driver"] = subprocess.run(["nvidia-smi", "--query-gpu=driver_version", "--format=csv,noheader", "-i", "0"],
+                                       capture_output=True, text=True, timeout=10).stdout.strip()
+    except Exception:
+        out["driver"] = None
+    return out
+
+
 def induced_prefix_subgraph(rp, ci, target_edges):
     """CPU-baseline sample: the subgraph induced by the first R nodes (R chosen so it holds about
     target_edges entries).  Keeps the generator's locality/community structure."""
@@ -255,15 +286,16 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record()
+    for i in range(args.steps):
         step()
-    e1.record()
+        ev[i + 1].record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = ev[0].elapsed_time(ev[-1]) / args.steps
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     stages = plan.timings()
     clk = clocks.stop() if rank == 0 else None
     if world > 1:
@@ -331,7 +363,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "nodes": n, "nnz": nnz, "heads": h, "head_dim": d,
                        "strategy": info["strategy_name"], "parallelism": f"graph-row x{world}",
-                       "l2": "inputs larger than L2 (K, V tables 1.25 GB each vs 126 MB L2); no flush",
+                       "l2": f"inputs larger than L2 (K, V tables {n * h * d * elt / 1e9:.2f} GB each vs 126 MB L2); "
+                             "no flush",
                        "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 1024,
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
                        "bwd_mode": info["bwd_mode"]},
@@ -344,6 +377,8 @@ def run_ours(args):
             "plan": {"t_gen_s": t_gen, "t_plan_s": t_plan, "heavy_rows": info["heavy_rows"],
                      "heavy_cols": info["heavy_cols"], "exch_fwd_bytes": info["exch_fwd_bytes"],
                      "exch_bwd_bytes": info["exch_bwd_bytes"], "predicted_ms": info["predicted_ms"]},
+            # SURVEY 8(d) report fields (rank 0's view; step times are this rank's CUDA events)
+            "report": report_fields(per_step, stages, info, world, nnz, step_bytes, peak),
         }
         print(json.dumps(line), flush=True)
     plan.close()

@@ -37,7 +37,7 @@
  *     CUDA faults surface as GT_ECUDA on a later call.
  *   - Collective calls (gt_plan, gt_attn_fwd, gt_attn_bwd with world > 1) must be made by every
  *     rank in the same order.  A plan is used by one host thread at a time.
- *   - Supported shapes: heads in {1,2,4,8}, heads*d in {128, 256, 512}, d >= 8 (bf16) / 4 (fp32).
+ *   - Supported shapes: heads in {1,2,4,8}, heads*d in {64, 128, 256, 512}.
  *     Others return GT_ECONFIG.
  */
 #ifndef GT_H_

@@ -422,7 +422,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   if (!csr->row_ptr || (nnz > 0 && !csr->col_idx)) return fail(GT_EINVAL, "gt_plan: null CSR arrays");
   if (heads <= 0 || d <= 0) return fail(GT_EINVAL, "gt_plan: heads and d must be positive");
   if (!shape_supported(heads, d, opts->dtype))
-    return fail(GT_ECONFIG, "gt_plan: unsupported shape: need heads in {1,2,4,8}, heads*d in {128,256,512}, "
+    return fail(GT_ECONFIG, "gt_plan: unsupported shape: need heads in {1,2,4,8}, heads*d in {64,128,256,512}, "
                             "dtype f32|bf16; got heads=" + std::to_string(heads) + " d=" + std::to_string(d));
   if (world < 1 || opts->rank < 0 || opts->rank >= world) return fail(GT_EINVAL, "gt_plan: bad world/rank");
   if (world > 1 && (!opts->comm || (opts->comm_kind != GT_COMM_NCCL && opts->comm_kind != GT_COMM_LOOPBACK)))

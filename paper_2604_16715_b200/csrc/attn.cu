@@ -256,6 +256,7 @@ gt_status merge_list(int dtype, int H, int D, int64_t nids, const int32_t* ids, 
 #define GT_CASE(TT, HH, DD) \
   if (H == HH && D == DD) return Merges<TT, HH, DD>::run_list(nids, ids, ptr, idx, part, dk, dv, scale, st);
 #define GT_HCASES(TT)                                                                              \
+  GT_CASE(TT, 1, 64) GT_CASE(TT, 2, 64) GT_CASE(TT, 4, 64) GT_CASE(TT, 8, 64)                        \
   GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
   GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
   GT_CASE(TT, 8, 256) GT_CASE(TT, 8, 512)
@@ -270,6 +271,7 @@ gt_status merge(int dtype, int H, int D, int pass, const MergeArgs& m, cudaStrea
 #define GT_CASE(TT, HH, DD) \
   if (H == HH && D == DD) return Merges<TT, HH, DD>::run(pass, m, st);
 #define GT_HCASES(TT)                                                                              \
+  GT_CASE(TT, 1, 64) GT_CASE(TT, 2, 64) GT_CASE(TT, 4, 64) GT_CASE(TT, 8, 64)                        \
   GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
   GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
   GT_CASE(TT, 8, 256) GT_CASE(TT, 8, 512)
@@ -286,7 +288,7 @@ bool shape_supported(int heads, int d, int dtype) {
   const int D = heads * d;
   if (dtype != GT_F32 && dtype != GT_BF16) return false;
   if (heads != 1 && heads != 2 && heads != 4 && heads != 8) return false;
-  return D == 128 || D == 256 || D == 512;
+  return D == 64 || D == 128 || D == 256 || D == 512;
 }
 
 int launches_fwd(const gt_plan_s* P) {

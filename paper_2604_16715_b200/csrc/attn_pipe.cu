@@ -123,7 +123,7 @@ struct PC {
   // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dP)[U][H]
   static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * 8 : 0);
   static constexpr int WARP_SMEM = kS * (STAGE + OWNP + XS);
-  static_assert(LB == 8 || LB % 16 == 0, "lane slice must be 8 bytes or a multiple of 16");
+  static_assert(LB == 4 || LB == 8 || LB % 16 == 0, "lane slice must be 4, 8 or a multiple of 16 bytes");
   static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
 };
 
@@ -163,7 +163,9 @@ struct PArgs {
 // lane slice copy of one row: LB bytes at byte offset lane * LB
 template <int LB>
 __device__ __forceinline__ void cp_slice(char* dst_row, const char* src_row, int lane) {
-  if constexpr (LB == 8) {
+  if constexpr (LB == 4) {
+    cp_async<4>(dst_row + lane * 4, src_row + lane * 4);
+  } else if constexpr (LB == 8) {
     cp_async<8>(dst_row + lane * 8, src_row + lane * 8);
   } else {
 #pragma unroll
@@ -181,7 +183,9 @@ __device__ __forceinline__ const char* row_addr(const char* base, uint32_t idx, 
 // this lane's LB bytes: dst and src already point at the lane's slice
 template <int LB>
 __device__ __forceinline__ void cp_lane_z(char* dst, const char* src, bool valid) {
-  if constexpr (LB == 8) {
+  if constexpr (LB == 4) {
+    cp_async4z(dst, src, valid);
+  } else if constexpr (LB == 8) {
     cp_async8z(dst, src, valid);
   } else {
 #pragma unroll
@@ -199,9 +203,11 @@ __device__ __forceinline__ void lds_f32(const char* p, float (&f)[EPL]) {
       uint4 x = *reinterpret_cast<const uint4*>(p + 16 * i);
       w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
     }
-  } else {
+  } else if constexpr (W == 2) {
     uint2 x = *reinterpret_cast<const uint2*>(p);
     w[0] = x.x; w[1] = x.y;
+  } else {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
   }
   if constexpr (sizeof(T) == 4) {
 #pragma unroll
@@ -233,8 +239,10 @@ __device__ __forceinline__ void stg_f32(char* p, const float (&f)[EPL]) {
 #pragma unroll
     for (int i = 0; i < W / 4; ++i)
       reinterpret_cast<uint4*>(p)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-  } else {
+  } else if constexpr (W == 2) {
     *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  } else {
+    *reinterpret_cast<uint32_t*>(p) = w[0];
   }
 }
 
@@ -276,9 +284,11 @@ __device__ __forceinline__ void lds_raw(const char* p, uint32_t (&w)[W]) {
       uint4 x = *reinterpret_cast<const uint4*>(p + 16 * i);
       w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
     }
-  } else {
+  } else if constexpr (W == 2) {
     uint2 x = *reinterpret_cast<const uint2*>(p);
     w[0] = x.x; w[1] = x.y;
+  } else {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
   }
 }
 
@@ -769,6 +779,7 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
 #define GT_HCASES(TT) GT_CASE(TT, 4, 256)
 #else
 #define GT_HCASES(TT)                                                                              \
+  GT_CASE(TT, 1, 64) GT_CASE(TT, 2, 64) GT_CASE(TT, 4, 64) GT_CASE(TT, 8, 64)                        \
   GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
   GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
   GT_CASE(TT, 8, 256) GT_CASE(TT, 8, 512)

@@ -141,7 +141,7 @@ def test_reduce_scatter_hub_columns_chunked_and_deterministic():
 
 # GP-A2A head parallelism (Alg. 2): heads / world heads of all rows per rank
 @pytest.mark.parametrize("world,h,d,dtype", [(2, 4, 64, "bf16"), (2, 8, 32, "f32"), (4, 8, 64, "f32"),
-                                             (4, 8, 64, "bf16")])
+                                             (4, 8, 64, "bf16"), (4, 4, 64, "bf16")])
 @pytest.mark.parametrize("edge_state", [1, -1])
 def test_loopback_a2a_head_parallel(world, h, d, dtype, edge_state):
     rp, ci = gtgen.random_graph(2200, 28000, seed=120 + world + h, directed=True, power=2.1)

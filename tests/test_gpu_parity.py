@@ -61,6 +61,7 @@ def test_c2_arxiv_bf16(gt):
 SHAPES = [  # h, d, dtype
     (4, 64, "bf16"), (4, 64, "f32"), (8, 16, "f32"), (8, 32, "bf16"), (1, 128, "bf16"), (2, 64, "f32"),
     (2, 256, "bf16"), (8, 64, "f32"), (1, 256, "f32"), (4, 32, "bf16"),
+    (1, 64, "bf16"), (4, 16, "bf16"), (8, 8, "f32"), (2, 32, "f32"),   # heads * d = 64 (4-byte bf16 lane slices)
 ]
 
 
