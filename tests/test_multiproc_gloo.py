@@ -119,3 +119,55 @@ def test_gloo_multirank_protocol(world, seed):
         p.join(timeout=60)
     for r in range(world):
         assert results.get(r) == "ok", results.get(r)
+
+
+def _agp_worker(rank, world, port, result_q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2604_16715_b200 import agp
+
+        beta, raw = agp.profile_beta(world, [2048, 8192, 32768], 256, torch.device("cpu"), reps=2)
+        if rank == 0:
+            for ci, c in enumerate(agp.COLLECTIVES):
+                for p in range(2, world + 1):
+                    assert beta[ci, p] > 0 and np.isfinite(beta[ci, p]), (c, p)
+                    assert [r for r, _ in raw[c][p]] == [2048, 8192, 32768]
+            # Alg. 3 on the profiled table: a huge t_iter(1) makes every candidate feasible (the argmin
+            # is then the smallest score), a tiny one none (single GPU, reading Z12)
+            big = agp.decide(1e6, 1e8, 1e6, beta)
+            scores = {(c, p): v["score"] for c, d in big["estimates"].items() for p, v in d.items()}
+            best = min(scores.values())
+            assert big["score"] == best and big["strategy"] in agp.COLLECTIVES and big["gpus"] >= 2
+            assert all(v["feasible"] for d in big["estimates"].values() for v in d.values())
+            small = agp.decide(1e6, 1e8, 1e-12, beta)
+            assert small["strategy"] == "single" and small["gpus"] == 1
+            # Eq. 7 / 8 estimate = t1 / p + beta N
+            est = big["estimates"]["allgather"][2]["t_iter_est_s"]
+            assert abs(est - (1e6 / 2 + beta[0, 2] * 1e6)) <= 1e-9 * est
+        dist.barrier()
+        dist.destroy_process_group()
+        result_q.put((rank, "ok"))
+    except Exception:
+        import traceback
+        result_q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_agp_beta_profile_and_selection(world):
+    """NEXT-2 driver (paper_2604_16715_b200.agp): Fig. 2-style beta sweeps over p = 2..world on a
+    gloo group, the log-log fit, and Alg. 3 / Eq. 7-8 on the profiled table."""
+    from paper_2604_16715_b200 import _build
+    _build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert results.get(r) == "ok", results.get(r)
