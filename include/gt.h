@@ -119,6 +119,15 @@ typedef struct {
                                    dK || dV of the remote columns its rows touch and sends them to the
                                    owners (all-gather: a reduce-scatter; halo: the reverse halo), which
                                    sum them in a fixed order.  2 D fp32 per exchanged row. */
+  int transport;           /* world > 1 forward K || V transport (strategies halo / all-gather):
+                              0 => pack + all-to-all-v / all-gather (NCCL or loopback) into a receive
+                                   table, on a side stream overlapped with the owned-column entries;
+                              1 => fused peer gather: every rank publishes its K || V
+                                   rows in a plan buffer shared with the peers (CUDA IPC for NCCL
+                                   ranks, one GPU per process, peer access over NVLink; the pointer
+                                   itself for loopback ranks) and the forward / row-pass kernels load
+                                   remote rows directly from the owners, with device-side barriers
+                                   instead of a copy.  Needs world <= 8 and bwd_mode = 0. */
 } gt_opts;
 
 typedef struct {
@@ -144,6 +153,7 @@ typedef struct {
   int edge_state;                 /* 1 if the plan materialises per-entry state (gt_opts.edge_state) */
   int64_t edge_state_bytes;       /* device bytes of that state */
   int bwd_mode;                   /* backward dataflow in use (gt_opts.bwd_mode; 0 when world == 1) */
+  int transport;                  /* forward K || V transport in use (gt_opts.transport) */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,

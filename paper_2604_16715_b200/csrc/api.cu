@@ -324,13 +324,15 @@ static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
   I.launches_fwd = launches_fwd(P) + (single ? 0 : 1);
   I.launches_bwd = launches_bwd(P) + (single ? 0 : (P->bwd_reduce ? 0 : 1));
   I.bwd_mode = P->bwd_reduce ? 1 : 0;
+  I.transport = P->peer ? 1 : 0;
+  if (P->peer) I.launches_fwd = launches_fwd(P) + 1;  // + the publish pack
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
                           &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src,
                           &P->d_hrow, &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx,
                           &P->d_hq, &P->d_hk, &P->d_hv, &P->d_hy, &P->d_hlse, &P->d_hdy, &P->d_hdq, &P->d_hdk,
-                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2]})
+                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2], &P->d_pub, &P->d_iota})
     dev += (int64_t)b->bytes;
   if (P->strategy == GT_A2A && P->sub) {  // the world-1 plan over all rows with heads / world heads
     const gt_plan_info& S = P->sub->info;
@@ -434,6 +436,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     return fail(GT_ECONFIG, "gt_plan: GP-A2A needs heads % world == 0 and a supported (heads / world, d) shape");
   if (opts->partition != 0 && opts->partition != 1) return fail(GT_EINVAL, "gt_plan: partition must be 0 or 1");
   if (opts->bwd_mode != 0 && opts->bwd_mode != 1) return fail(GT_EINVAL, "gt_plan: bwd_mode must be 0 or 1");
+  if (opts->transport != 0 && opts->transport != 1) return fail(GT_EINVAL, "gt_plan: transport must be 0 or 1");
+  if (world > 1 && opts->transport == 1 && (world > 8 || opts->bwd_mode == 1))
+    return fail(GT_ECONFIG, "gt_plan: the peer-gather transport needs world <= 8 and the transposed-owner backward");
   if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
   if (opts->validate) GT_TRY(validate_csr(csr->row_ptr, csr->col_idx, n, nnz));
   else if (csr->row_ptr[n] != nnz) return fail(GT_EGRAPH, "row_ptr[n] != nnz");
@@ -669,7 +674,24 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   if (!single) {
     const bool ag = P->strategy == GT_ALLGATHER;
     cols.assign(csr->col_idx + csr->row_ptr[P->lo], csr->col_idx + csr->row_ptr[P->hi]);
-    remap_ids(cols.data(), (int64_t)cols.size(), P.get(), P->halo_out, ag);
+    P->peer = opts->transport == 1 && P->strategy != GT_A2A;
+    if (P->peer) {  // remote column j -> n_local + (owner << shift) + (j - bounds[owner])
+      while ((int64_t(1) << P->peer_shift) < std::max<int64_t>(P->n_max, 2)) ++P->peer_shift;
+      if (P->n_local + ((int64_t)world << P->peer_shift) >= (int64_t(1) << 31))
+        return fail(GT_ECONFIG, "gt_plan: peer-gather ids do not fit in 32 bits");
+#pragma omp parallel for schedule(static)
+      for (int64_t e = 0; e < (int64_t)cols.size(); ++e) {
+        const int64_t j = cols[(size_t)e];
+        if (j >= P->lo && j < P->hi) {
+          cols[(size_t)e] = (int32_t)(j - P->lo);
+        } else {
+          const int o = owner_of(P->bounds, j);
+          cols[(size_t)e] = (int32_t)(P->n_local + ((int64_t)o << P->peer_shift) + (j - P->bounds[o]));
+        }
+      }
+    } else {
+      remap_ids(cols.data(), (int64_t)cols.size(), P.get(), P->halo_out, ag);
+    }
     GT_TRY(upload(P->d_col, cols.data(), cols.size()));
     std::vector<int32_t> rows((size_t)P->nnz_in_local);
     if (P->nnz_in_local)
@@ -691,7 +713,16 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     int64_t sbytes = std::max((int64_t)f.send_idx.size(), (int64_t)b.send_idx.size()) * P->kv_row_bytes;
     if (ag) sbytes = P->n_max * P->kv_row_bytes;
     GT_TRY(P->d_send_buf.alloc((size_t)std::max<int64_t>(sbytes, 16)));
-    GT_TRY(P->d_recv_kv.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
+    if (P->peer) {
+      GT_TRY(P->d_pub.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->kv_row_bytes));
+      std::vector<int32_t> iota((size_t)P->n_local);
+      std::iota(iota.begin(), iota.end(), 0);
+      GT_TRY(upload(P->d_iota, iota.data(), iota.size()));
+      GT_TRY(P->comm->share_pointers(P->d_pub.p, P->peer_base, st));
+      GT_TRY(P->d_recv_kv.alloc(16));
+    } else {
+      GT_TRY(P->d_recv_kv.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
+    }
     if (!P->bwd_reduce) {  // transposed-owner backward: [q | dy] and (LSE2, D) rows of the in-halo
       GT_TRY(P->d_recv_qd.alloc((size_t)std::max<int64_t>(b.recv_rows * P->kv_row_bytes, 16)));
       GT_TRY(P->d_recv_st.alloc((size_t)std::max<int64_t>(b.recv_rows * P->st_row_bytes, 16)));
@@ -933,6 +964,13 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   }
   const void* halo = nullptr;
   cudaEvent_t ev = nullptr, ev2 = nullptr;
+  if (P->peer) {  // fused peer gather: no exchange, the kernels read remote rows from the owners
+    P->mark_begin(1, st, &ev);
+    GT_TRY(launch_fwd_peer(P, q, k, v, y, lse, st));
+    P->mark_end(1, st, ev);
+    P->fwd_done = true;
+    return GT_OK;
+  }
   if (P->world > 1) {
     // K||V rows of the halo on the side stream, overlapped with phase A (owned-column entries)
     const int elt = P->dtype == GT_F32 ? 4 : 2;
@@ -980,7 +1018,8 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
     P->mark_end(3, st, e1);
     return GT_OK;
   }
-  const void* halo_kv = P->world > 1 ? P->d_recv_kv.p : nullptr;
+  // remote K || V rows: the received table, or (peer gather) the owners' published rows
+  const void* halo_kv = P->world > 1 ? (P->peer ? P->d_pub.p : P->d_recv_kv.p) : nullptr;
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   const bool multi = P->world > 1;
   const bool ag = P->strategy == GT_ALLGATHER;

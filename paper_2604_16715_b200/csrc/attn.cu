@@ -350,6 +350,31 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
   return GT_OK;
 }
 
+// Forward with the fused peer-gather transport: own rows published, owned-column entries (phase A)
+// while the peers publish, a device-side barrier, then remote-column entries (phase B) reading the
+// owners' rows over NVLink.  The first barrier keeps a rank from overwriting its published rows while
+// peers may still read them (their previous row pass).
+gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void* v, void* y, float* lse,
+                          cudaStream_t st) {
+  const int elt = P->dtype == GT_F32 ? 4 : 2;
+  float* part = P->d_part_fwd.as<float>();
+  const ChunkTable& ct = P->fwd_chunks;
+  GT_TRY(P->comm->stream_barrier(st));
+  GT_TRY(pack_kv(k, v, P->d_iota.as<int32_t>(), P->n_local, (int64_t)P->heads * P->d, elt, P->d_pub.p, st));
+  GT_TRY(pipe_pass(P, 0, P->w_fwd[0], ct, part, q, nullptr, nullptr, k, v, nullptr, nullptr, y, nullptr, lse, st, 0,
+                   entry_state(P, 0)));
+  GT_TRY(P->comm->stream_barrier(st));
+  GT_TRY(pipe_pass(P, 0, P->w_fwd[1], ct, part, q, nullptr, nullptr, k, v, P->d_pub.p, nullptr, y, nullptr, lse, st,
+                   0, entry_state(P, 0)));
+  if (ct.nchunks() > 0) {
+    MergeArgs m = merge_args(ct, P->d_part_fwd, P->scale);
+    m.y = (char*)y;
+    m.lse = lse;
+    GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 0, m, st));
+  }
+  return GT_OK;
+}
+
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st) {
   GT_TRY(pipe_pass(P, 1, P->w_rows, P->heavy_rows, P->d_part_rowb.as<float>(), q, dy, lse, k, v, halo_kv, nullptr,

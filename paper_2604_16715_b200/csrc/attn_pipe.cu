@@ -140,6 +140,8 @@ struct PArgs {
   const char* gb;        // local tensor gathered second (v | v | dy)
   const char* gs;        // local (LSE2, D) rows [n_local][SB bytes] (pass 2)
   const char* halo;      // packed remote rows: [k | v] (passes 0, 1) or [q | dy] (pass 2)
+  const char* peer[8];   // fused peer gather (passes 0, 1; peer_shift > 0): rank s's published [k | v] rows
+  int peer_shift;        //   remote slot = (owner << peer_shift) + offset
   const char* halo_s;    // pass 2: remote (LSE2, D) blocks [rows][SB bytes]
   int64_t halo_stride;
   int64_t n_local;
@@ -480,7 +482,13 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       const char *pa, *pb, *ps = nullptr;
       if constexpr (HALO) {
         const bool loc = cv < n_loc;
-        const char* hrow = row_addr(h_l, cv - n_loc, 2 * RB);
+        const char* hrow;
+        if (PASS < 2 && a.peer_shift) {  // NVLink peer load of the owner's published row (kernel param: uniform)
+          const uint32_t slot = cv - n_loc;
+          hrow = row_addr(a.peer[(slot >> a.peer_shift) & 7] + lane * LB, slot & ((1u << a.peer_shift) - 1), 2 * RB);
+        } else {
+          hrow = row_addr(h_l, cv - n_loc, 2 * RB);
+        }
         pa = loc ? row_addr(ga_l, cv, RB) : hrow;
         pb = loc ? row_addr(gb_l, cv, RB) : hrow + RB;
         if constexpr (PASS == 2) ps = loc ? row_addr(gs_l, cv, C::SB) : row_addr(hs_l, cv - n_loc, C::SB);
@@ -826,6 +834,8 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.part = part;
   a.qscale = P->scale * pipe::kLog2e;
   a.scale = P->scale;
+  a.peer_shift = (P->peer && pass < 2 && halo) ? P->peer_shift : 0;
+  for (int s = 0; s < 8; ++s) a.peer[s] = (const char*)P->peer_base[s];
   a.es_out = es.out;
   a.es_in = es.in;
   a.src = es.src;

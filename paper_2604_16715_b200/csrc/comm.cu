@@ -237,6 +237,39 @@ struct NcclComm : Comm {
     double x = 0;
     return max_host(&x, stream);
   }
+  gt_status stream_barrier(cudaStream_t stream) override {
+    // an all-reduce of one word completes on no rank before every rank has entered it
+    GT_TRY(ensure_scratch());
+    GT_NCCL_TRY(nccl().AllReduce((char*)scratch.p + 2048, (char*)scratch.p + 2048, 1, ncclInt32, ncclSum, c, stream));
+    return GT_OK;
+  }
+  std::vector<void*> opened;  // IPC mappings to close
+  gt_status share_pointers(void* local, void** peers, cudaStream_t stream) override {
+    GT_TRY(ensure_scratch());
+    if ((int64_t)sizeof(cudaIpcMemHandle_t) * w > 2048) return fail(GT_ECONFIG, "share_pointers: world too large");
+    cudaIpcMemHandle_t mine;
+    GT_CUDA_TRY(cudaIpcGetMemHandle(&mine, local));
+    GT_CUDA_TRY(cudaMemcpyAsync((char*)scratch.p + r * sizeof(mine), &mine, sizeof(mine), cudaMemcpyHostToDevice,
+                                stream));
+    GT_NCCL_TRY(nccl().AllGather((char*)scratch.p + r * sizeof(mine), scratch.p, sizeof(mine), ncclUint8, c, stream));
+    std::vector<cudaIpcMemHandle_t> all((size_t)w);
+    GT_CUDA_TRY(cudaMemcpyAsync(all.data(), scratch.p, sizeof(mine) * w, cudaMemcpyDeviceToHost, stream));
+    GT_CUDA_TRY(cudaStreamSynchronize(stream));
+    for (int s = 0; s < w; ++s) {
+      if (s == r) {
+        peers[s] = local;
+        continue;
+      }
+      void* p = nullptr;
+      GT_CUDA_TRY(cudaIpcOpenMemHandle(&p, all[(size_t)s], cudaIpcMemLazyEnablePeerAccess));
+      opened.push_back(p);
+      peers[s] = p;
+    }
+    return GT_OK;
+  }
+  ~NcclComm() override {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
 };
 
 }  // namespace
@@ -267,6 +300,7 @@ struct gt_loopback_s {
     cudaEvent_t ready = nullptr, done = nullptr;
     std::vector<char> host;
     double val = 0;
+    void* ptr = nullptr;
   };
   std::vector<Slot> slots;
   void barrier() {
@@ -361,6 +395,22 @@ struct LoopbackComm : Comm {
     return GT_OK;
   }
   gt_status barrier(cudaStream_t) override {
+    g->barrier();
+    return GT_OK;
+  }
+  gt_status stream_barrier(cudaStream_t stream) override {
+    GT_CUDA_TRY(cudaEventRecord(ready, stream));
+    g->slots[r].ready = ready;
+    g->barrier();
+    for (int s = 0; s < g->world; ++s)
+      if (s != r) GT_CUDA_TRY(cudaStreamWaitEvent(stream, g->slots[s].ready, 0));
+    g->barrier();  // nobody re-records its event before every rank has enqueued its waits
+    return GT_OK;
+  }
+  gt_status share_pointers(void* local, void** peers, cudaStream_t) override {
+    g->slots[r].ptr = local;
+    g->barrier();
+    for (int s = 0; s < g->world; ++s) peers[s] = g->slots[s].ptr;
     g->barrier();
     return GT_OK;
   }

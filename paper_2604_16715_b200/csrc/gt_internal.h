@@ -62,6 +62,12 @@ struct Comm {
   // max over ranks of a host double (host-synchronous).
   virtual gt_status max_host(double* v, cudaStream_t stream) = 0;
   virtual gt_status barrier(cudaStream_t stream) = 0;
+  // device-side barrier enqueued on `stream`: work after it on any rank's stream starts only once every
+  // rank's stream has reached it (no host synchronisation).
+  virtual gt_status stream_barrier(cudaStream_t stream) = 0;
+  // collective, host-synchronous: peers[s] = an address of rank s's device buffer `local` valid in this
+  // process (CUDA IPC for one process per GPU; the pointer itself for in-process ranks).
+  virtual gt_status share_pointers(void* local, void** peers, cudaStream_t stream) = 0;
 };
 
 Comm* make_nccl_comm(void* nccl_comm, int world, int rank, gt_status* st);
@@ -182,6 +188,17 @@ struct gt_plan_s {
   cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr, ev_fwd0 = nullptr, ev_halo = nullptr;
   bool fwd_done = false;
 
+  // fused peer-gather transport (opts.transport = 1): every rank publishes its K || V
+  // rows in d_pub; the forward's remote-column entries and the row pass read remote rows straight from
+  // the owners' publish buffers (NVLink peer loads by the attention kernels themselves, overlapped with
+  // the math) instead of a pack + exchange + receive copy.  Remote column ids are
+  // n_local + (owner << peer_shift) + offset.
+  bool peer = false;
+  int peer_shift = 0;
+  void* peer_base[8] = {};
+  gt::DevBuf d_pub;                // [n_local][k | v]
+  gt::DevBuf d_iota;               // int32 [n_local] 0, 1, ...
+
   // GP-A2A head-parallel strategy (Alg. 2): a world-1 plan over
   // the full graph with heads / world heads; Q, K, V, dY, LSE are scattered by head group (all-to-all,
   // rows of this rank -> all rows of this rank's heads), Y, LSE, dQ, dK, dV gathered back.  The head
@@ -214,6 +231,9 @@ namespace gt {
 // attention kernels (attn.cu)
 gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv, void* y,
                      float* lse, cudaStream_t st, cudaEvent_t halo_ready);
+// forward with the fused peer-gather transport
+gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void* v, void* y, float* lse,
+                          cudaStream_t st);
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
                           const float* lse, const void* dy, void* dq, cudaStream_t st);
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,

@@ -40,7 +40,7 @@ class _Opts(ctypes.Structure):
                 ("dtype", ctypes.c_int), ("scale", ctypes.c_float), ("strategy", ctypes.c_int),
                 ("validate", ctypes.c_int), ("partition", ctypes.c_int), ("device", ctypes.c_int),
                 ("heavy_threshold", ctypes.c_int), ("beta_profile", ctypes.c_char_p), ("profile", ctypes.c_int),
-                ("edge_state", ctypes.c_int), ("bwd_mode", ctypes.c_int)]
+                ("edge_state", ctypes.c_int), ("bwd_mode", ctypes.c_int), ("transport", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -54,7 +54,8 @@ class _Info(ctypes.Structure):
                 + [("beta_s_per_row", ctypes.c_double * 5), ("predicted_ms", ctypes.c_double * 5),
                    ("agp_score", ctypes.c_double * 5), ("agp_feasible", ctypes.c_int * 5),
                    ("alpha_s_per_unit", ctypes.c_double), ("edge_state", ctypes.c_int),
-                   ("edge_state_bytes", ctypes.c_int64), ("bwd_mode", ctypes.c_int)])
+                   ("edge_state_bytes", ctypes.c_int64), ("bwd_mode", ctypes.c_int),
+                   ("transport", ctypes.c_int)])
 
 
 _lib = None
@@ -263,7 +264,7 @@ class Plan:
     def __init__(self, row_ptr, col_idx, heads: int, d: int, dtype="bf16", scale: float = 0.0, world: int = 1,
                  rank: int = 0, comm=None, strategy="auto", heavy_threshold: int = 0, partition: int = 0,
                  validate: bool = True, device: int = -1, profile: bool = False, edge_state: int = 0,
-                 bwd_mode: int = 0):
+                 bwd_mode: int = 0, transport: int = 0):
         L = lib()
         self.row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         self.col_idx = np.ascontiguousarray(col_idx, np.int32)
@@ -282,6 +283,7 @@ class Plan:
         opts.profile = int(profile)
         opts.edge_state = int(edge_state)
         opts.bwd_mode = int(bwd_mode)
+        opts.transport = int(transport)
         if world > 1:
             if isinstance(comm, LoopbackGroup):
                 opts.comm_kind, opts.comm = GT_COMM_LOOPBACK, comm.handle

@@ -18,7 +18,8 @@ from tests._util import TOL, check_lse, inputs, normwise, to_f64, to_torch
 pytestmark = pytest.mark.gpu
 
 
-def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0, bwd_mode=0):
+def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0, bwd_mode=0,
+                 transport=0, steps=1):
     import torch
     import paper_2604_16715_b200 as gt
     n = len(rp) - 1
@@ -35,13 +36,14 @@ def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=
             s = torch.cuda.Stream()
             plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, world=world, rank=r, comm=grp,
                            strategy=strategy, heavy_threshold=heavy, partition=partition, edge_state=edge_state,
-                           bwd_mode=bwd_mode)
+                           bwd_mode=bwd_mode, transport=transport)
             lo, hi = plan.row_lo, plan.row_hi
             with torch.cuda.stream(s):
                 tq, tk, tv, tdy = (t[lo:hi].contiguous() for t in full)
             s.synchronize()
-            y, lse = plan.fwd(tq, tk, tv, stream=s)
-            dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy, stream=s)
+            for _ in range(steps):  # repeated steps exercise the reuse of exchange / publish buffers
+                y, lse = plan.fwd(tq, tk, tv, stream=s)
+                dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy, stream=s)
             s.synchronize()
             ex = {w: plan.export(w) for w in ("bounds", "halo_out", "halo_in")}
             ex["send_out"] = [plan.export("send_out", p) for p in range(world)]
@@ -170,3 +172,29 @@ def test_loopback_auto_considers_a2a():
     for r in res:
         assert np.isfinite(r[4]["predicted_ms"][4])  # GP-A2A probed and costed
     assert len({r[4]["strategy_name"] for r in res}) == 1
+
+
+# fused peer gather (transport 1): kernels read remote K || V rows from the owners'
+# published buffers (loopback ranks share one device, so peer pointers are plain device pointers)
+@pytest.mark.parametrize("edge_state", [1, -1])
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("strategy", ["halo", "allgather"])
+def test_loopback_peer_gather(world, strategy, edge_state):
+    rp, ci = gtgen.random_graph(2600, 32000, seed=140 + world, directed=True, power=2.1)
+    ins, res = run_loopback(rp, ci, 4, 64, "bf16", world, strategy, seed=1400 + world, heavy=64,
+                            edge_state=edge_state, transport=1, steps=3)
+    check(rp, ci, "bf16", ins, res, world)
+    for r in res:
+        assert r[4]["transport"] == 1
+
+
+def test_peer_gather_config_errors():
+    import paper_2604_16715_b200 as gt
+    rp, ci = gtgen.random_graph(300, 2000, seed=6, power=2.3)
+    grp = gt.LoopbackGroup(2)
+    try:
+        with pytest.raises(gt.GTError) as e:  # rejected before any collective
+            gt.Plan(rp, ci, 4, 64, dtype="f32", world=2, rank=0, comm=grp, strategy="halo", transport=1, bwd_mode=1)
+        assert e.value.status == 3
+    finally:
+        grp.close()
