@@ -203,9 +203,11 @@ gt_status gt_attn_bwd(gt_plan_t plan, const void* q, const void* k, const void* 
                       const void* dy, void* dq, void* dk, void* dv, void* stream);
 
 /* End-to-end step with HOST buffers (pinned for full speed): copies q, k, v, dy host->device,
- * runs gt_attn_fwd and gt_attn_bwd, copies y, lse, dq, dk, dv device->host, and synchronises
- * `stream`.  Device staging buffers are allocated on first use and owned by the plan.
- * Any output pointer may be NULL to skip its copy. */
+ * runs gt_attn_fwd and gt_attn_bwd, copies y, lse, dq, dk, dv device->host, and returns when all of
+ * it is done.  The copies run on two plan-owned copy streams ordered by events against `stream`
+ * (PCIe is full duplex): k, v, q in, then the forward while dy arrives; y and lse go out during the
+ * backward, dq during the column pass, dk and dv last.  Device staging buffers are allocated on
+ * first use and owned by the plan.  Any output pointer may be NULL to skip its copy. */
 gt_status gt_attn_fwd_bwd_host(gt_plan_t plan, const void* q, const void* k, const void* v, const void* dy,
                                void* y, float* lse, void* dq, void* dk, void* dv, void* stream);
 

@@ -205,6 +205,11 @@ gt_plan_s::~gt_plan_s() {
   for (auto& r : recs) { ev_pool.push_back(r.a); ev_pool.push_back(r.b); }
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
+  if (e2e_in) cudaStreamDestroy(e2e_in);
+  if (e2e_out) cudaStreamDestroy(e2e_out);
+  for (cudaEvent_t e : e2e_ev)
+    if (e) cudaEventDestroy(e);
+  if (ev_dq) cudaEventDestroy(ev_dq);
   if (comm && own_comm) delete comm;
   delete sub;
 }
@@ -1028,6 +1033,7 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
     // owners on the side stream while the owned columns run; then the fixed-order merge.
     P->mark_begin(2, st, &ev);
     GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
+    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecord(P->ev_dq_ready, st));
     GT_TRY(launch_bwd_halo_cols(P, q, dy, st));
     P->mark_end(2, st, ev);
     GT_CUDA_TRY(cudaEventRecord(P->ev_rows, st));
@@ -1061,6 +1067,7 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   }
   P->mark_begin(2, st, &ev);
   GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
+  if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecord(P->ev_dq_ready, st));
   P->mark_end(2, st, ev);
   if (multi) {
     // (LSE2, D) blocks of the in-halo rows: written by the row pass on their owners
@@ -1098,17 +1105,46 @@ gt_status gt_attn_fwd_bwd_host(gt_plan_t P, const void* q, const void* k, const 
     if (!P->h2d[i].p) GT_TRY(P->h2d[i].alloc(i == 5 ? lb : tb));
   const size_t nb = (size_t)P->n_local * P->heads * P->d * elt;
   const size_t nl = (size_t)P->n_local * P->heads * sizeof(float);
-  const void* in[4] = {q, k, v, dy};
-  for (int i = 0; i < 4; ++i)
-    if (nb) GT_CUDA_TRY(cudaMemcpyAsync(P->h2d[i].p, in[i], nb, cudaMemcpyHostToDevice, st));
+  // Copies overlap the compute on two copy streams (PCIe is full duplex): K, V, Q in; the forward
+  // starts when they are resident while dY is still arriving; Y, LSE go out during the backward, dQ
+  // during the column pass, dK, dV last.
+  if (!P->e2e_in) {
+    GT_CUDA_TRY(cudaStreamCreateWithFlags(&P->e2e_in, cudaStreamNonBlocking));
+    GT_CUDA_TRY(cudaStreamCreateWithFlags(&P->e2e_out, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&P->e2e_ev[0], &P->e2e_ev[1], &P->e2e_ev[2], &P->e2e_ev[3], &P->e2e_ev[4], &P->ev_dq})
+      GT_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_start = P->e2e_ev[0], ev_qkv = P->e2e_ev[1], ev_dy = P->e2e_ev[2], ev_fwd = P->e2e_ev[3],
+              ev_bwd = P->e2e_ev[4];
+  GT_CUDA_TRY(cudaEventRecord(ev_start, st));  // staging buffers are free once earlier work on `stream` is
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_in, ev_start, 0));
+  const void* in[4] = {k, v, q, dy};
+  const int in_idx[4] = {1, 2, 0, 3};
+  for (int i = 0; i < 4; ++i) {
+    if (nb) GT_CUDA_TRY(cudaMemcpyAsync(P->h2d[in_idx[i]].p, in[i], nb, cudaMemcpyHostToDevice, P->e2e_in));
+    if (i == 2) GT_CUDA_TRY(cudaEventRecord(ev_qkv, P->e2e_in));
+  }
+  GT_CUDA_TRY(cudaEventRecord(ev_dy, P->e2e_in));
+  GT_CUDA_TRY(cudaStreamWaitEvent(st, ev_qkv, 0));
   GT_TRY(gt_attn_fwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[4].p, P->h2d[5].as<float>(), stream));
-  GT_TRY(gt_attn_bwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[5].as<float>(), P->h2d[3].p, P->h2d[6].p,
-                     P->h2d[7].p, P->h2d[8].p, stream));
-  void* outs[5] = {y, lse, dq, dk, dv};
-  const int idx[5] = {4, 5, 6, 7, 8};
-  for (int i = 0; i < 5; ++i)
-    if (outs[i] && nb)
-      GT_CUDA_TRY(cudaMemcpyAsync(outs[i], P->h2d[idx[i]].p, idx[i] == 5 ? nl : nb, cudaMemcpyDeviceToHost, st));
+  GT_CUDA_TRY(cudaEventRecord(ev_fwd, st));
+  GT_CUDA_TRY(cudaStreamWaitEvent(st, ev_dy, 0));
+  P->ev_dq_ready = P->ev_dq;
+  gt_status bs = gt_attn_bwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[5].as<float>(), P->h2d[3].p,
+                             P->h2d[6].p, P->h2d[7].p, P->h2d[8].p, stream);
+  P->ev_dq_ready = nullptr;
+  GT_TRY(bs);
+  if (P->strategy == GT_A2A) GT_CUDA_TRY(cudaEventRecord(P->ev_dq, st));  // dQ arrives with dK, dV there
+  GT_CUDA_TRY(cudaEventRecord(ev_bwd, st));
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev_fwd, 0));
+  if (y && nb) GT_CUDA_TRY(cudaMemcpyAsync(y, P->h2d[4].p, nb, cudaMemcpyDeviceToHost, P->e2e_out));
+  if (lse && nl) GT_CUDA_TRY(cudaMemcpyAsync(lse, P->h2d[5].p, nl, cudaMemcpyDeviceToHost, P->e2e_out));
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, P->ev_dq, 0));
+  if (dq && nb) GT_CUDA_TRY(cudaMemcpyAsync(dq, P->h2d[6].p, nb, cudaMemcpyDeviceToHost, P->e2e_out));
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev_bwd, 0));
+  if (dk && nb) GT_CUDA_TRY(cudaMemcpyAsync(dk, P->h2d[7].p, nb, cudaMemcpyDeviceToHost, P->e2e_out));
+  if (dv && nb) GT_CUDA_TRY(cudaMemcpyAsync(dv, P->h2d[8].p, nb, cudaMemcpyDeviceToHost, P->e2e_out));
+  GT_CUDA_TRY(cudaStreamSynchronize(P->e2e_out));
   GT_CUDA_TRY(cudaStreamSynchronize(st));
   return GT_OK;
 }

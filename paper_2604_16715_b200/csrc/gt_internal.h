@@ -210,8 +210,11 @@ struct gt_plan_s {
   gt::DevBuf d_stage[3];                                                  // [world][n_local] head-group rows
   std::vector<int64_t> a2a_loc_off, a2a_loc_cnt, a2a_glob_off, a2a_glob_cnt;  // per peer, in rows
 
-  // end-to-end host staging
+  // end-to-end host staging (gt_attn_fwd_bwd_host): copy streams and their ordering events
   gt::DevBuf h2d[9];
+  cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
+  cudaEvent_t e2e_ev[5] = {}, ev_dq = nullptr;
+  cudaEvent_t ev_dq_ready = nullptr;  // when set, gt_attn_bwd records it once dQ is complete
 
   gt_plan_info info{};
   cudaStream_t side = nullptr;
