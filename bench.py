@@ -321,7 +321,11 @@ def run_ours(args):
         pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "alg_bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom]}
+                "alg_bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom],
+                # the DRAM bytes ncu measured for this kernel (profiles/, cold cache) over its live launch
+                # time: real HBM utilisation, as opposed to the no-reuse algorithmic model above
+                "dram_achieved": (traffic / (stage_ms[dom] * 1e-3) / 1e9) if traffic else None,
+                "dram_frac": (traffic / (stage_ms[dom] * 1e-3) / 1e9 / peak) if traffic else None}
 
     # ---- end to end through the C ABI with pinned host buffers ----
     e2e = None
