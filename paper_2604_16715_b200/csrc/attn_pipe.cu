@@ -46,7 +46,7 @@ constexpr unsigned kFull = 0xffffffffu;
 #define GT_PIPE_STAGES 2
 #endif
 #ifndef GT_PIPE_GRAB
-#define GT_PIPE_GRAB 4
+#define GT_PIPE_GRAB 1
 #endif
 constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
 constexpr int kS = GT_PIPE_STAGES;      // stages per warp (2 measured best: more resident warps)
