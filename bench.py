@@ -36,7 +36,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
     ap.add_argument("--strategy", default=None, help="auto|allgather|halo (world > 1)")
-    ap.add_argument("--heavy", type=int, default=0, help="heavy row/column threshold (0 = library default)")
+    ap.add_argument("--heavy", type=int, default=int(os.environ.get("GT_HEAVY", "0")),
+                    help="heavy row/column threshold (0 = library default)")
     ap.add_argument("--edge-state", type=int, default=int(os.environ.get("GT_EDGE_STATE", "0")),
                     help="gt_opts.edge_state: 0 auto (materialise when it fits), 1 on, -1 recompute")
     ap.add_argument("--bwd-mode", type=int, default=0,
@@ -369,7 +370,7 @@ def run_ours(args):
                        "strategy": info["strategy_name"], "parallelism": f"graph-row x{world}",
                        "l2": f"inputs larger than L2 (K, V tables {n * h * d * elt / 1e9:.2f} GB each vs 126 MB L2); "
                              "no flush",
-                       "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 1024,
+                       "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 512,
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
                        "bwd_mode": info["bwd_mode"]},
             "roofline": roofline,

@@ -102,7 +102,7 @@ typedef struct {
   int validate;            /* 1 => O(n + nnz) CSR checks in gt_plan (GT_EGRAPH on failure) */
   int partition;           /* 0 => rows+edges balanced (reading Z9), 1 => node-balanced */
   int device;              /* CUDA device ordinal; -1 => the calling thread's current device */
-  int heavy_threshold;     /* rows/columns with more entries are split into chunks; 0 => 1024 */
+  int heavy_threshold;     /* rows/columns with more entries are split into chunks; 0 => 512 */
   const char* beta_profile;/* optional path of a measured-beta JSON; NULL => probe at plan time */
   int profile;             /* 1 => record CUDA events around every stage (gt_plan_timings) */
   int edge_state;          /* per-entry state of the backward (Table 1 keeps U per edge,

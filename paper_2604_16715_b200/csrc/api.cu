@@ -461,7 +461,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   P->n = n;
   P->nnz = nnz;
   P->scale = opts->scale > 0.f ? opts->scale : (float)(1.0 / std::sqrt((double)heads * d));
-  P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 1024;
+  P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 512;  // A/B-tuned on C3
   P->profile = opts->profile != 0;
   P->bwd_reduce = world > 1 && opts->bwd_mode == 1;
   P->stats_stride = (int)((8 * heads + 15) / 16 * 16 / 4);
