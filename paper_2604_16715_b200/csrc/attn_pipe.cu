@@ -114,7 +114,11 @@ struct PC {
   static constexpr int OWN_DY = PASS == 1 ? RB : 0;
   static constexpr int OWN_LSE = OWN_DY + RB;
   static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * H : ((ES & 1) ? 0 : 2 * RB));
+#ifdef GT_PIPE_U  // tuning override (A/B builds)
+  static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : (GT_PIPE_U * H <= 32 ? GT_PIPE_U : 32 / H));
+#else
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
+#endif
   // per-stage entry state gathered into the stage (ES): rowb s2[U][H] f32 (the forward's logits),
   // colb (P, dP)[U][H] f32x2 (the row pass's)
   static constexpr int AUX = PASS == 1 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 2 && (ES & 1)) ? U * H * 8 : 0);
