@@ -24,10 +24,18 @@
  *
  * Multi-GPU (Alg. 1 GP-AG, generalised): rank r owns rows [row_lo, row_hi) of every
  * [N, h, d] tensor.  Remote K||V rows needed by its edges are fetched by an all-gather
- * (GT_ALLGATHER) or by a halo exchange of only the cut-edge columns (GT_HALO); the backward
- * fetches Q||dY||(LSE, D) of in-neighbour rows the same way and each owner computes dK, dV of
- * its own columns ("transposed-owner", reading Z11).  GT_AUTO picks the strategy with the cost
- * model of Eq. 6-8 over measured exchange times (Alg. 3, at fixed world).
+ * (GT_ALLGATHER) or by a halo exchange of only the cut-edge columns (GT_HALO) — as copies into a
+ * receive table (gt_opts.transport = 0) or loaded by the kernels straight from the owners over
+ * NVLink (transport = 1).  The backward either fetches Q||dY||(LSE, D) of in-neighbour rows the
+ * same way and each owner computes dK, dV of its own columns ("transposed-owner", reading Z11), or
+ * sends fp32 partial dK||dV to the owners (gt_opts.bwd_mode = 1, the paper's reduce-scatter).
+ * GT_A2A is the paper's head-parallel GP-A2A (Alg. 2).  GT_AUTO picks the strategy with
+ * the cost model of Eq. 6-8 over measured exchange times (Alg. 3, at fixed
+ * world).
+ *
+ * Per-entry state (gt_opts.edge_state, on by default when it fits): the forward keeps each entry's
+ * logit and the row pass its (P, dP) (Table 1 keeps Z and U per edge), so the
+ * backward does not recompute them.
  *
  * Conventions
  *   - All functions return gt_status; they never abort or throw.  The message of the last

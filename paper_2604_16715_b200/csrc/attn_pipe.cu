@@ -29,6 +29,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "gt_internal.h"
@@ -739,6 +740,8 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     GT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, smem));
+    if (const char* cap = std::getenv("GT_CTAS_PER_SM"))  // tuning: narrower in-flight window of rows
+      per = std::min(per, std::max(1, std::atoi(cap)));
     grid = sms * std::max(per, 1);
   }
   if (a.nitems <= 0) return GT_OK;

@@ -117,13 +117,14 @@ def test_loopback_communities_f32_auto(bwd_mode):
     assert len(chosen) == 1 and chosen <= {"halo", "allgather"}  # every rank applies rank 0's decision
 
 
-@pytest.mark.parametrize("bwd_mode", [0, 1])
-def test_loopback_more_ranks_than_rows_and_node_partition(bwd_mode):
+@pytest.mark.parametrize("bwd_mode,transport", [(0, 0), (1, 0), (0, 1)])
+def test_loopback_more_ranks_than_rows_and_node_partition(bwd_mode, transport):
     rp, ci = gtgen.csr_from_pairs(3, [(0, 1), (1, 2), (2, 0), (2, 1)])
-    ins, res = run_loopback(rp, ci, 2, 64, "f32", 5, "halo", seed=901, bwd_mode=bwd_mode)
+    ins, res = run_loopback(rp, ci, 2, 64, "f32", 5, "halo", seed=901, bwd_mode=bwd_mode, transport=transport)
     check(rp, ci, "f32", ins, res, 5)
     rp, ci = gtgen.random_graph(700, 6000, seed=91, power=2.3)
-    ins, res = run_loopback(rp, ci, 4, 32, "bf16", 3, "allgather", seed=902, partition=1, bwd_mode=bwd_mode)
+    ins, res = run_loopback(rp, ci, 4, 32, "bf16", 3, "allgather", seed=902, partition=1, bwd_mode=bwd_mode,
+                            transport=transport)
     check(rp, ci, "bf16", ins, res, 3, partition=1)
 
 
