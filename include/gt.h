@@ -127,15 +127,17 @@ typedef struct {
                                    dK || dV of the remote columns its rows touch and sends them to the
                                    owners (all-gather: a reduce-scatter; halo: the reverse halo), which
                                    sum them in a fixed order.  2 D fp32 per exchanged row. */
-  int transport;           /* world > 1 forward K || V transport (strategies halo / all-gather):
+  int transport;           /* world > 1 transport of remote rows (strategies halo / all-gather):
                               0 => pack + all-to-all-v / all-gather (NCCL or loopback) into a receive
                                    table, on a side stream overlapped with the owned-column entries;
                               1 => fused peer gather: every rank publishes its K || V
-                                   rows in a plan buffer shared with the peers (CUDA IPC for NCCL
-                                   ranks, one GPU per process, peer access over NVLink; the pointer
-                                   itself for loopback ranks) and the forward / row-pass kernels load
-                                   remote rows directly from the owners, with device-side barriers
-                                   instead of a copy.  Needs world <= 8 and bwd_mode = 0. */
+                                   rows (forward) and Q || dY rows (backward) in plan buffers shared
+                                   with the peers, and shares its (LSE, D) array in place (CUDA IPC
+                                   for NCCL ranks, one GPU per process, peer access over NVLink; the
+                                   pointer itself for loopback ranks); the forward / row-pass /
+                                   column-pass kernels load remote rows directly from the owners,
+                                   with device-side barriers instead of copies.  Needs world <= 8
+                                   and bwd_mode = 0. */
 } gt_opts;
 
 typedef struct {

@@ -337,7 +337,7 @@ static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
                           &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src,
                           &P->d_hrow, &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx,
                           &P->d_hq, &P->d_hk, &P->d_hv, &P->d_hy, &P->d_hlse, &P->d_hdy, &P->d_hdq, &P->d_hdk,
-                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2], &P->d_pub, &P->d_iota})
+                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2], &P->d_pub, &P->d_iota, &P->d_pub_qd})
     dev += (int64_t)b->bytes;
   if (P->strategy == GT_A2A && P->sub) {  // the world-1 plan over all rows with heads / world heads
     const gt_plan_info& S = P->sub->info;
@@ -702,7 +702,20 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     if (P->nnz_in_local)
       GT_CUDA_TRY(cudaMemcpy(rows.data(), full_row.as<int32_t>() + c0, rows.size() * sizeof(int32_t),
                              cudaMemcpyDeviceToHost));
-    remap_ids(rows.data(), (int64_t)rows.size(), P.get(), P->halo_in, ag);
+    if (P->peer) {  // remote row i -> n_local + (owner << shift) + (i - bounds[owner])
+#pragma omp parallel for schedule(static)
+      for (int64_t e = 0; e < (int64_t)rows.size(); ++e) {
+        const int64_t i = rows[(size_t)e];
+        if (i >= P->lo && i < P->hi) {
+          rows[(size_t)e] = (int32_t)(i - P->lo);
+        } else {
+          const int o = owner_of(P->bounds, i);
+          rows[(size_t)e] = (int32_t)(P->n_local + ((int64_t)o << P->peer_shift) + (i - P->bounds[o]));
+        }
+      }
+    } else {
+      remap_ids(rows.data(), (int64_t)rows.size(), P.get(), P->halo_in, ag);
+    }
     GT_TRY(upload(P->d_row, rows.data(), rows.size()));
     GT_TRY(upload(P->d_col_ptr, P->h_col_ptr.data(), P->h_col_ptr.size()));
     const Pattern& f = ag ? pf_ag : pf_halo;
@@ -724,11 +737,13 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       std::iota(iota.begin(), iota.end(), 0);
       GT_TRY(upload(P->d_iota, iota.data(), iota.size()));
       GT_TRY(P->comm->share_pointers(P->d_pub.p, P->peer_base, st));
+      GT_TRY(P->d_pub_qd.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->kv_row_bytes));
+      GT_TRY(P->comm->share_pointers(P->d_pub_qd.p, P->peer_qd, st));
       GT_TRY(P->d_recv_kv.alloc(16));
     } else {
       GT_TRY(P->d_recv_kv.alloc((size_t)std::max<int64_t>(f.recv_rows * P->kv_row_bytes, 16)));
     }
-    if (!P->bwd_reduce) {  // transposed-owner backward: [q | dy] and (LSE2, D) rows of the in-halo
+    if (!P->bwd_reduce && !P->peer) {  // transposed-owner backward: [q | dy] and (LSE2, D) rows of the in-halo
       GT_TRY(P->d_recv_qd.alloc((size_t)std::max<int64_t>(b.recv_rows * P->kv_row_bytes, 16)));
       GT_TRY(P->d_recv_st.alloc((size_t)std::max<int64_t>(b.recv_rows * P->st_row_bytes, 16)));
       GT_TRY(P->d_send_st.alloc((size_t)std::max<int64_t>((ag ? P->n_max : (int64_t)b.send_idx.size()) * P->st_row_bytes, 16)));
@@ -851,6 +866,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * (2 * D + heads) * sizeof(float)));
   GT_TRY(P->d_part_colb.alloc((size_t)std::max<int64_t>(ncc, 1) * (2 * D) * sizeof(float)));
   GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->stats_stride * sizeof(float)));
+  if (P->peer) GT_TRY(P->comm->share_pointers(P->d_stats.p, P->peer_st, st));  // read by the peers' column pass
   GT_CUDA_TRY(cudaStreamSynchronize(st));
 
   fill_info(P.get(), nrc, ncc);
@@ -913,7 +929,10 @@ gt_status gt_plan_export(gt_plan_t P, int what, int peer, void* dst, int64_t cap
         for (auto& x : tmp32) {
           int64_t i = x;
           if (i < P->n_local) x = (int32_t)(i + P->lo);
-          else if (P->strategy == GT_ALLGATHER) {
+          else if (P->peer) {
+            const int64_t slot = i - P->n_local;
+            x = (int32_t)(P->bounds[slot >> P->peer_shift] + (slot & ((int64_t(1) << P->peer_shift) - 1)));
+          } else if (P->strategy == GT_ALLGATHER) {
             int64_t s = (i - P->n_local) / P->n_max, off = (i - P->n_local) % P->n_max;
             x = (int32_t)(P->bounds[s] + off);
           } else {
@@ -1046,6 +1065,22 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
     GT_CUDA_TRY(cudaEventRecord(P->ev_side, P->side));
     P->mark_begin(4, st, &ev);
     GT_TRY(launch_bwd_cols_rs(P, q, k, v, dy, dk, dv, st, P->ev_side));
+    P->mark_end(4, st, ev);
+    return GT_OK;
+  }
+  if (multi && P->peer) {
+    // Fused peer gather, backward: publish [q | dy] (known at entry) once every peer is done with the
+    // previous step's rows, row pass (its (LSE2, D) stats are read in place by the peers), owned-row
+    // column entries, a device-side barrier, then the remote-row column entries read from the owners.
+    const int elt = P->dtype == GT_F32 ? 4 : 2;
+    P->mark_begin(2, st, &ev);
+    GT_TRY(P->comm->stream_barrier(st));
+    GT_TRY(pack_kv(q, dy, P->d_iota.as<int32_t>(), P->n_local, (int64_t)P->heads * P->d, elt, P->d_pub_qd.p, st));
+    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
+    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecord(P->ev_dq_ready, st));
+    P->mark_end(2, st, ev);
+    P->mark_begin(4, st, &ev);
+    GT_TRY(launch_bwd_cols_peer(P, q, k, v, dy, dk, dv, st));
     P->mark_end(4, st, ev);
     return GT_OK;
   }

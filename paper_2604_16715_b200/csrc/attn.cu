@@ -350,6 +350,33 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
   return GT_OK;
 }
 
+// Column pass with the fused peer-gather transport: owned-row entries first (split plans) or nothing,
+// a device-side barrier (every rank's [q | dy] rows are published and its row pass has written the
+// (LSE2, D) blocks), then the entries with remote rows, read from the owners.
+gt_status launch_bwd_cols_peer(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy, void* dk,
+                               void* dv, cudaStream_t st) {
+  const ChunkTable& ct = P->col_split ? P->col_chunks : P->heavy_cols;
+  float* part = P->d_part_colb.as<float>();
+  const void* mark = P->d_pub_qd.p;  // non-null: selects the remote-row (peer) kernel
+  if (!P->col_split) {
+    GT_TRY(P->comm->stream_barrier(st));
+    GT_TRY(pipe_pass(P, 2, P->w_cols, ct, part, k, v, nullptr, q, dy, mark, mark, dk, dv, nullptr, st, 0,
+                     entry_state(P, 2)));
+  } else {
+    GT_TRY(pipe_pass(P, 2, P->w_colp[0], ct, part, k, v, nullptr, q, dy, nullptr, nullptr, dk, dv, nullptr, st, 0,
+                     entry_state(P, 2)));
+    GT_TRY(P->comm->stream_barrier(st));
+    GT_TRY(pipe_pass(P, 2, P->w_colp[1], ct, part, k, v, nullptr, q, dy, mark, mark, dk, dv, nullptr, st, 0));
+  }
+  if (ct.nchunks() > 0) {
+    MergeArgs m = merge_args(ct, P->d_part_colb, P->scale);
+    m.dk = (char*)dk;
+    m.dv = (char*)dv;
+    GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 2, m, st));
+  }
+  return GT_OK;
+}
+
 // Forward with the fused peer-gather transport: own rows published, owned-column entries (phase A)
 // while the peers publish, a device-side barrier, then remote-column entries (phase B) reading the
 // owners' rows over NVLink.  The first barrier keeps a rank from overwriting its published rows while

@@ -145,7 +145,8 @@ struct PArgs {
   const char* gb;        // local tensor gathered second (v | v | dy)
   const char* gs;        // local (LSE2, D) rows [n_local][SB bytes] (pass 2)
   const char* halo;      // packed remote rows: [k | v] (passes 0, 1) or [q | dy] (pass 2)
-  const char* peer[8];   // fused peer gather (passes 0, 1; peer_shift > 0): rank s's published [k | v] rows
+  const char* peer[8];   // fused peer gather (peer_shift > 0): rank s's published rows, [k | v] (passes 0,
+  const char* peer_s[8]; //   1) or [q | dy] (pass 2), and (pass 2) rank s's (LSE2, D) blocks
   int peer_shift;        //   remote slot = (owner << peer_shift) + offset
   const char* halo_s;    // pass 2: remote (LSE2, D) blocks [rows][SB bytes]
   int64_t halo_stride;
@@ -488,15 +489,19 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       if constexpr (HALO) {
         const bool loc = cv < n_loc;
         const char* hrow;
-        if (PASS < 2 && a.peer_shift) {  // NVLink peer load of the owner's published row (kernel param: uniform)
+        const char* srow = nullptr;
+        if (a.peer_shift) {  // NVLink peer load of the owner's published row (kernel param: uniform)
           const uint32_t slot = cv - n_loc;
-          hrow = row_addr(a.peer[(slot >> a.peer_shift) & 7] + lane * LB, slot & ((1u << a.peer_shift) - 1), 2 * RB);
+          const uint32_t own = (slot >> a.peer_shift) & 7, off = slot & ((1u << a.peer_shift) - 1);
+          hrow = row_addr(a.peer[own] + lane * LB, off, 2 * RB);
+          if constexpr (PASS == 2) srow = row_addr(a.peer_s[own] + lane * 16, off, C::SB);
         } else {
           hrow = row_addr(h_l, cv - n_loc, 2 * RB);
+          if constexpr (PASS == 2) srow = row_addr(hs_l, cv - n_loc, C::SB);
         }
         pa = loc ? row_addr(ga_l, cv, RB) : hrow;
         pb = loc ? row_addr(gb_l, cv, RB) : hrow + RB;
-        if constexpr (PASS == 2) ps = loc ? row_addr(gs_l, cv, C::SB) : row_addr(hs_l, cv - n_loc, C::SB);
+        if constexpr (PASS == 2) ps = loc ? row_addr(gs_l, cv, C::SB) : srow;
       } else {
         pa = row_addr(ga_l, cv, RB);
         pb = row_addr(gb_l, cv, RB);
@@ -841,8 +846,11 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.part = part;
   a.qscale = P->scale * pipe::kLog2e;
   a.scale = P->scale;
-  a.peer_shift = (P->peer && pass < 2 && halo) ? P->peer_shift : 0;
-  for (int s = 0; s < 8; ++s) a.peer[s] = (const char*)P->peer_base[s];
+  a.peer_shift = (P->peer && halo) ? P->peer_shift : 0;
+  for (int s = 0; s < 8; ++s) {
+    a.peer[s] = (const char*)(pass < 2 ? P->peer_base[s] : P->peer_qd[s]);
+    a.peer_s[s] = (const char*)P->peer_st[s];
+  }
   a.es_out = es.out;
   a.es_in = es.in;
   a.src = es.src;

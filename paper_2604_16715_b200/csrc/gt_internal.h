@@ -198,6 +198,9 @@ struct gt_plan_s {
   void* peer_base[8] = {};
   gt::DevBuf d_pub;                // [n_local][k | v]
   gt::DevBuf d_iota;               // int32 [n_local] 0, 1, ...
+  gt::DevBuf d_pub_qd;             // [n_local][q | dy]: the backward's published rows
+  void* peer_qd[8] = {};           // per rank: its d_pub_qd
+  void* peer_st[8] = {};           // per rank: its d_stats ((LSE2, D) blocks, written by its row pass)
 
   // GP-A2A head-parallel strategy (Alg. 2): a world-1 plan over
   // the full graph with heads / world heads; Q, K, V, dY, LSE are scattered by head group (all-to-all,
@@ -234,6 +237,9 @@ namespace gt {
 // attention kernels (attn.cu)
 gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv, void* y,
                      float* lse, cudaStream_t st, cudaEvent_t halo_ready);
+// column pass with the fused peer-gather transport (remote in-neighbour rows read from the owners)
+gt_status launch_bwd_cols_peer(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy, void* dk,
+                               void* dv, cudaStream_t st);
 // forward with the fused peer-gather transport
 gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void* v, void* y, float* lse,
                           cudaStream_t st);
