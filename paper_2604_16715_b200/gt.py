@@ -259,7 +259,16 @@ def _dtype_code(dtype) -> int:
 
 
 class Plan:
-    """A gt_plan_t: the graph prepared for sparse attention on this rank's device."""
+    """A gt_plan_t: the graph prepared for sparse attention on this rank's device (gt_plan).
+
+    row_ptr / col_idx: the GLOBAL CSR (int64 / int32), identical on every rank.  heads, d: the
+    [N, heads, d] layout of every feature tensor.  Options map one to one onto gt_opts (include/gt.h):
+    dtype "bf16" | "f32"; scale (0 -> 1 / sqrt(heads d)); world / rank / comm (LoopbackGroup or
+    NcclComm) for multi-rank plans; strategy "auto" | "single" | "allgather" | "halo" | "a2a";
+    heavy_threshold (0 -> 512); partition 0 (rows + edges) | 1 (nodes); edge_state 0 | 1 | -1
+    (materialised logits and (P, dP): auto / on / off); bwd_mode 0 (transposed owner) | 1
+    (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); profile (per-stage CUDA events).
+    """
 
     def __init__(self, row_ptr, col_idx, heads: int, d: int, dtype="bf16", scale: float = 0.0, world: int = 1,
                  rank: int = 0, comm=None, strategy="auto", heavy_threshold: int = 0, partition: int = 0,
