@@ -69,7 +69,8 @@ typedef enum {
   GT_ENOMEM = 4,   /* device or host allocation failed */
   GT_ECUDA = 5,    /* CUDA runtime error (possibly from earlier asynchronous work) */
   GT_ENCCL = 6,    /* NCCL error, NCCL unavailable, or collective protocol mismatch */
-  GT_ESTATE = 7    /* call out of order (e.g. gt_attn_bwd before any gt_attn_fwd with world > 1) */
+  GT_ESTATE = 7    /* call out of order (gt_attn_bwd before any gt_attn_fwd on a plan that retains
+                      forward state: world > 1, entry-state logits, GP-A2A) */
 } gt_status;
 
 typedef enum { GT_F32 = 0, GT_BF16 = 1 } gt_dtype;
@@ -208,7 +209,10 @@ gt_status gt_attn_fwd(gt_plan_t plan, const void* q, const void* k, const void* 
 
 /* Backward.  q, k, v, lse as passed to / produced by the matching gt_attn_fwd; dy: device
  * [n_local, heads, d] upstream gradient.  dq, dk, dv: device [n_local, heads, d] outputs (same
- * dtype, round-to-nearest-even from fp32 accumulation).  Collective when world > 1. */
+ * dtype, round-to-nearest-even from fp32 accumulation).  Collective when world > 1.
+ * The plan retains state of the LAST gt_attn_fwd it ran (the received K||V rows when world > 1, the
+ * per-entry logits with edge_state, the head slices with GT_A2A): gt_attn_bwd uses it and returns
+ * GT_ESTATE when no gt_attn_fwd has run on this plan and such state is needed. */
 gt_status gt_attn_bwd(gt_plan_t plan, const void* q, const void* k, const void* v, const float* lse,
                       const void* dy, void* dq, void* dk, void* dv, void* stream);
 

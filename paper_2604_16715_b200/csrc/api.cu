@@ -1022,7 +1022,9 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
 gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse, const void* dy,
                       void* dq, void* dk, void* dv, void* stream) {
   GT_TRY(check_ptrs(P, {q, k, v, lse, dy, dq, dk, dv}));
-  if (P->world > 1 && !P->fwd_done) return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd (halo K||V not retained)");
+  if ((P->world > 1 || P->es_logits) && !P->fwd_done)
+    return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd: the plan uses the forward's retained state "
+                           "(received K||V rows, per-entry logits or GP-A2A head slices)");
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
   if (P->strategy == GT_A2A) {  // GP-A2A: scatter dY and LSE, all rows for this rank's heads, gather grads

@@ -180,3 +180,11 @@ def test_errors_are_reported(gt):
     with pytest.raises(gt.GTError) as e:
         gt.Plan(rp, ci, 4, 64, edge_state=2)
     assert e.value.status == 1  # GT_EINVAL
+    # backward before any forward on a plan with entry-state logits: the retained state is missing
+    import torch
+    plan = gt.Plan(rp, ci, 4, 64, dtype="f32", edge_state=1)
+    z = torch.zeros((4, 4, 64), dtype=torch.float32, device="cuda")
+    with pytest.raises(gt.GTError) as e:
+        plan.bwd(z, z, z, torch.zeros((4, 4), dtype=torch.float32, device="cuda"), z)
+    assert e.value.status == 7  # GT_ESTATE
+    plan.close()
