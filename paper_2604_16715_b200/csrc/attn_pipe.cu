@@ -1,29 +1,39 @@
 // Pipelined sparse-attention kernels for sm_100a: asynchronous gathers (cp.async / LDGSTS) of
 // neighbour rows into per-warp shared-memory stage rings.
 //
-// Same mathematics as the reference kernels in attn.cu (Eq. 2/4/5, Section 2.2):
+// Mathematics (Eq. 2/4/5, Section 2.2), base-2 softmax with fp32 accumulation:
 //   pass 0 (fwd):  per row i:    s_e = scale <q_i,k_j>, online softmax, y_i = sum p_e v_j / l, LSE
 //   pass 1 (rowb): per row i:    p_e = exp(s_e - LSE_i), dP_e = <dY_i, v_j>, D_i = sum p dP,
 //                                dQ_i = scale (sum p dP k_j - D_i sum p k_j)
-//   pass 2 (colb): per column j: p_e, dP_e recomputed from (q_i, dY_i, LSE_i, D_i);
-//                                dV_j = sum p dY_i, dK_j = scale sum p (dP - D_i) q_i
+//   pass 2 (colb): per column j: dV_j = sum p dY_i, dK_j = scale sum p (dP - D_i) q_i
+//
+// Entry state (template bits ES; Table 1 keeps Z and U per edge): with bit 2 the
+// forward stores each entry's base-2 logit and the row pass reads it instead of q.k; with bit 1 the
+// row pass stores (p, dP) per entry and the column pass reads them (through the CSC -> CSR map)
+// instead of recomputing q.k and dY.v.  Stores go through a per-warp shared-memory transpose: one
+// coalesced, predicated store per stage.  Without entry state the column pass recomputes p and dP
+// from (q_i, dY_i, LSE_i, D_i) and its own k_j, v_j.
+//
+// Remote rows (HALO kernels, world > 1) come from a received table, or (peer transport) straight
+// from the owners' published buffers through a per-rank base table (NVLink peer loads).
 //
 // Execution model.  Persistent CTAs; every warp owns a ring of kS stages in shared memory, each
-// holding up to U neighbours (two feature rows, plus the neighbour's (LSE2, D) pair in pass 2), and
-// an "own" slot per stage for the data of the row (column) an item starts.  Warps grab batches of
-// kG consecutive work items (rows, or chunks of heavy rows, in row order) with one atomicAdd, so the
-// resident warps sweep the graph in a narrow window of rows and the neighbours they gather stay in
-// L2 (community locality); consecutive items have contiguous edge ranges, streamed through a
-// 32-entry register window of neighbour ids with the next window prefetched.
+// holding up to U neighbours (two feature rows, plus the neighbour's (LSE2, D) pair in pass 2, plus
+// the stage's entry state), and an "own" slot per stage for the data of the row (column) an item
+// starts.  Warps grab kG consecutive work items (rows, or chunks of heavy rows, in row order) per
+// atomicAdd (kG = 1, A/B-tuned), so the resident warps sweep the graph in a narrow window of rows and
+// the neighbours they gather stay in L2 (community locality); consecutive items have contiguous
+// entry ranges, streamed through a 32-entry register window of neighbour ids with the next window
+// prefetched.  Rows with more than the plan's threshold of entries are split into chunks whose fp32
+// partial states are merged in chunk order by attn.cu (deterministic).
 //
 // The warp is its own producer.  Lane l issues cp.async copies of ITS 16-byte slice of every
 // gathered row (a whole 512-byte row is one coalesced request per warp) and later reads back only
 // those same bytes, so completion needs no barrier or cross-lane synchronisation: one
 // cp.async.commit_group per stage and cp.async.wait_group(kS - 1) before consuming the oldest
-// stage.  kS * U neighbours (16 KB at D = 256 bf16) stay in flight per warp, across row boundaries,
-// without occupying registers.  (A TMA cp.async.bulk variant - one lane issuing whole-row copies on
-// an mbarrier - was measured 2x slower: the per-lane UBLKCP issue loop and barrier traffic made it
-// instruction bound.)
+// stage.  kS * U neighbours (8 KB at D = 256 bf16) stay in flight per warp, across row boundaries,
+// without occupying registers.  (Measured alternatives - a TMA cp.async.bulk variant, lane-group
+// producers, half-warp rows - are in DESIGN.md section 6.)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
