@@ -139,6 +139,11 @@ typedef struct {
                                    column-pass kernels load remote rows directly from the owners,
                                    with device-side barriers instead of copies.  Needs world <= 8
                                    and bwd_mode = 0. */
+  int cuda_graphs;         /* 1 => world-1 plans replay their launch sequence as CUDA graphs (the
+                              first call of each direction runs eagerly; later calls are captured
+                              once per set of tensor pointers, up to 4, and replayed).  Not used on
+                              the legacy default stream or with profile = 1.  Small graphs, whose
+                              steps are launch-bound, gain most. */
 } gt_opts;
 
 typedef struct {

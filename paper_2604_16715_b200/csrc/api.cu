@@ -210,6 +210,8 @@ gt_plan_s::~gt_plan_s() {
   for (cudaEvent_t e : e2e_ev)
     if (e) cudaEventDestroy(e);
   if (ev_dq) cudaEventDestroy(ev_dq);
+  for (auto* c : {&gfwd, &gbwd})
+    for (auto& e : *c) cudaGraphExecDestroy(e.exec);
   if (comm && own_comm) delete comm;
   delete sub;
 }
@@ -464,6 +466,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 512;  // A/B-tuned on C3
   P->profile = opts->profile != 0;
   P->bwd_reduce = world > 1 && opts->bwd_mode == 1;
+  P->graphs = opts->cuda_graphs != 0;
   P->stats_stride = (int)((8 * heads + 15) / 16 * 16 / 4);
   const int64_t D = (int64_t)heads * d;
   const int elt = opts->dtype == GT_F32 ? 4 : 2;
@@ -965,8 +968,8 @@ static gt_status check_ptrs(gt_plan_t P, std::initializer_list<const void*> ps) 
   return GT_OK;
 }
 
-gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse, void* stream) {
-  GT_TRY(check_ptrs(P, {q, k, v, y, lse}));
+static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse,
+                                void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
   if (P->strategy == GT_A2A) {  // GP-A2A (Alg. 2): scatter Q, K, V by head group, all rows, gather Y, LSE
@@ -1019,12 +1022,8 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   return GT_OK;
 }
 
-gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse, const void* dy,
-                      void* dq, void* dk, void* dv, void* stream) {
-  GT_TRY(check_ptrs(P, {q, k, v, lse, dy, dq, dk, dv}));
-  if ((P->world > 1 || P->es_logits) && !P->fwd_done)
-    return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd: the plan uses the forward's retained state "
-                           "(received K||V rows, per-entry logits or GP-A2A head slices)");
+static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse,
+                                const void* dy, void* dq, void* dk, void* dv, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
   if (P->strategy == GT_A2A) {  // GP-A2A: scatter dY and LSE, all rows for this rank's heads, gather grads
@@ -1126,6 +1125,81 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   GT_TRY(launch_bwd_cols(P, q, k, v, dy, multi ? P->d_recv_qd.p : nullptr, multi ? P->d_recv_st.p : nullptr, dk,
                          dv, st, multi ? P->ev_side : nullptr));
   P->mark_end(4, st, ev);
+  return GT_OK;
+}
+
+// CUDA-graph replay of a world-1 plan's launch sequence (gt_opts.cuda_graphs): the first call of a
+// direction runs eagerly (kernel attributes, grid sizes), later calls are captured once per set of
+// tensor pointers and replayed (a few launches instead of ~10 driver calls; helps small graphs,
+// whose steps are launch-bound).  Not used for the legacy default stream, with profiling, or when
+// world > 1 (host-side protocol steps).
+static bool graph_ok(gt_plan_t P, cudaStream_t st, bool warm) {
+  return P->graphs && P->world == 1 && !P->profile && warm && st != nullptr && st != cudaStreamLegacy &&
+         st != cudaStreamPerThread;
+}
+
+}  // extern "C" (the template below has C++ linkage)
+template <typename F>
+static gt_status graph_run(gt_plan_t P, std::vector<gt_plan_s::GraphEntry>& cache, const gt_plan_s::GraphKey& key,
+                           cudaStream_t st, F&& eager) {
+  for (auto& e : cache)
+    if (e.key == key) {
+      GT_CUDA_TRY(cudaGraphLaunch(e.exec, st));
+      return GT_OK;
+    }
+  cudaGraph_t g = nullptr;
+  GT_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const gt_status s = eager();
+  const cudaError_t ce = cudaStreamEndCapture(st, &g);
+  if (s != GT_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  if (ce != cudaSuccess) return fail(GT_ECUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess) return fail(GT_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+  if (cache.size() >= 4) {  // a few pointer sets (allocator reuse makes steps repeat them)
+    cudaGraphExecDestroy(cache.front().exec);
+    cache.erase(cache.begin());
+  }
+  cache.push_back({key, exec});
+  GT_CUDA_TRY(cudaGraphLaunch(exec, st));
+  return GT_OK;
+}
+extern "C" {
+
+gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse, void* stream) {
+  GT_TRY(check_ptrs(P, {q, k, v, y, lse}));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (graph_ok(P, st, P->fwd_warm)) {
+    GT_CUDA_TRY(cudaSetDevice(P->device));
+    const gt_plan_s::GraphKey key = {q, k, v, y, lse, nullptr, nullptr, nullptr, nullptr, nullptr};
+    GT_TRY(graph_run(P, P->gfwd, key, st, [&] { return attn_fwd_eager(P, q, k, v, y, lse, stream); }));
+    P->fwd_done = true;
+    return GT_OK;
+  }
+  GT_TRY(attn_fwd_eager(P, q, k, v, y, lse, stream));
+  P->fwd_warm = true;
+  return GT_OK;
+}
+
+gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse, const void* dy,
+                      void* dq, void* dk, void* dv, void* stream) {
+  GT_TRY(check_ptrs(P, {q, k, v, lse, dy, dq, dk, dv}));
+  if ((P->world > 1 || P->es_logits) && !P->fwd_done)
+    return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd: the plan uses the forward's retained state "
+                           "(received K||V rows, per-entry logits or GP-A2A head slices)");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (graph_ok(P, st, P->bwd_warm)) {
+    GT_CUDA_TRY(cudaSetDevice(P->device));
+    const gt_plan_s::GraphKey key = {q, k, v, lse, dy, dq, dk, dv, P->ev_dq_ready, nullptr};
+    return graph_run(P, P->gbwd, key, st,
+                     [&] { return attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream); });
+  }
+  GT_TRY(attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream));
+  P->bwd_warm = true;
   return GT_OK;
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
 #include <functional>
 #include <string>
 #include <vector>
@@ -218,6 +219,15 @@ struct gt_plan_s {
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
   cudaEvent_t e2e_ev[5] = {}, ev_dq = nullptr;
   cudaEvent_t ev_dq_ready = nullptr;  // when set, gt_attn_bwd records it once dQ is complete
+
+  // CUDA-graph replay (gt_opts.cuda_graphs, world 1): executable graphs keyed by the tensor pointers
+  bool graphs = false, fwd_warm = false, bwd_warm = false;
+  typedef std::array<const void*, 10> GraphKey;
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> gfwd, gbwd;
 
   gt_plan_info info{};
   cudaStream_t side = nullptr;

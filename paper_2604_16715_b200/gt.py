@@ -40,7 +40,8 @@ class _Opts(ctypes.Structure):
                 ("dtype", ctypes.c_int), ("scale", ctypes.c_float), ("strategy", ctypes.c_int),
                 ("validate", ctypes.c_int), ("partition", ctypes.c_int), ("device", ctypes.c_int),
                 ("heavy_threshold", ctypes.c_int), ("beta_profile", ctypes.c_char_p), ("profile", ctypes.c_int),
-                ("edge_state", ctypes.c_int), ("bwd_mode", ctypes.c_int), ("transport", ctypes.c_int)]
+                ("edge_state", ctypes.c_int), ("bwd_mode", ctypes.c_int), ("transport", ctypes.c_int),
+                ("cuda_graphs", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -267,13 +268,14 @@ class Plan:
     NcclComm) for multi-rank plans; strategy "auto" | "single" | "allgather" | "halo" | "a2a";
     heavy_threshold (0 -> 512); partition 0 (rows + edges) | 1 (nodes); edge_state 0 | 1 | -1
     (materialised logits and (P, dP): auto / on / off); bwd_mode 0 (transposed owner) | 1
-    (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); profile (per-stage CUDA events).
+    (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); cuda_graphs (world-1 graph
+    replay); profile (per-stage CUDA events).
     """
 
     def __init__(self, row_ptr, col_idx, heads: int, d: int, dtype="bf16", scale: float = 0.0, world: int = 1,
                  rank: int = 0, comm=None, strategy="auto", heavy_threshold: int = 0, partition: int = 0,
                  validate: bool = True, device: int = -1, profile: bool = False, edge_state: int = 0,
-                 bwd_mode: int = 0, transport: int = 0):
+                 bwd_mode: int = 0, transport: int = 0, cuda_graphs: bool = False):
         L = lib()
         self.row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         self.col_idx = np.ascontiguousarray(col_idx, np.int32)
@@ -293,6 +295,7 @@ class Plan:
         opts.edge_state = int(edge_state)
         opts.bwd_mode = int(bwd_mode)
         opts.transport = int(transport)
+        opts.cuda_graphs = int(cuda_graphs)
         if world > 1:
             if isinstance(comm, LoopbackGroup):
                 opts.comm_kind, opts.comm = GT_COMM_LOOPBACK, comm.handle

@@ -188,3 +188,38 @@ def test_errors_are_reported(gt):
         plan.bwd(z, z, z, torch.zeros((4, 4), dtype=torch.float32, device="cuda"), z)
     assert e.value.status == 7  # GT_ESTATE
     plan.close()
+
+
+def test_cuda_graph_replay_matches_eager(gt):
+    """gt_opts.cuda_graphs: captured and replayed steps (two pointer sets, the cache keyed by them)
+    give bitwise the eager results and stay within tolerance of the oracle."""
+    import torch
+    rp, ci = gtgen.random_graph(1500, 20000, seed=71, power=2.2)
+    h, d = 4, 64
+    q, k, v, dy = inputs(1500, h, d, "bf16", 701)
+    scale = 1.0 / math.sqrt(h * d)
+    tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
+    eager = gt.Plan(rp, ci, h, d, dtype="bf16", scale=scale, heavy_threshold=64)
+    y0, l0 = eager.fwd(tq, tk, tv)
+    g0 = eager.bwd(tq, tk, tv, l0, tdy)
+    s = torch.cuda.Stream()
+    plan = gt.Plan(rp, ci, h, d, dtype="bf16", scale=scale, heavy_threshold=64, cuda_graphs=True)
+    outs = []
+    with torch.cuda.stream(s):
+        bufs = [(torch.empty_like(tq), torch.empty((1500, h), dtype=torch.float32, device="cuda")) for _ in range(2)]
+        gbufs = [tuple(torch.empty_like(tq) for _ in range(3)) for _ in range(2)]
+    for it in range(5):  # eager warm-up, capture set 0, capture set 1, replay 0, replay 1
+        y, lse = bufs[it % 2]
+        dq, dk, dv = gbufs[it % 2]
+        plan.fwd(tq, tk, tv, y, lse, stream=s)
+        plan.bwd(tq, tk, tv, lse, tdy, dq, dk, dv, stream=s)
+        s.synchronize()
+        outs.append(tuple(t.clone() for t in (y, lse, dq, dk, dv)))
+    torch.cuda.synchronize()
+    ref = (y0, l0) + tuple(g0)
+    for o in outs:
+        for a, b in zip(o, ref):
+            assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
+                               b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
+    Y, _ = oracle.forward(rp, ci, q, k, v, scale)
+    assert normwise(to_f64(outs[-1][0]), Y) <= 2e-2
