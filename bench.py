@@ -167,14 +167,37 @@ def induced_prefix_subgraph(rp, ci, target_edges):
     return sub_rp, cols[keep].astype(np.int32), R
 
 
-def oracle_step(sub_rp, sub_ci, R, cfg, seed, scale):
+def oracle_step(sub_rp, sub_ci, R, cfg, seed, scale, keep=False):
     import gtgen
     import oracle
     q, k, v, dy = (gtgen.features(seed, nm, R, cfg.heads, cfg.d, cfg.dtype) for nm in ("q", "k", "v", "dy"))
     t0 = time.perf_counter()
-    oracle.forward(sub_rp, sub_ci, q, k, v, scale)
-    oracle.backward(sub_rp, sub_ci, q, k, v, dy, scale)
-    return time.perf_counter() - t0
+    Y, _ = oracle.forward(sub_rp, sub_ci, q, k, v, scale)
+    DQ, DK, DV, _ = oracle.backward(sub_rp, sub_ci, q, k, v, dy, scale)
+    t = time.perf_counter() - t0
+    return (t, (q, k, v, dy), (Y, DQ, DK, DV)) if keep else t
+
+
+def sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs):
+    """Normwise errors (reading Z8) of the CUDA path against the oracle on the CPU-baseline sample."""
+    import numpy as np
+    import torch
+    h, d = cfg.heads, cfg.d
+    conv = ((lambda x: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda()) if cfg.dtype == "bf16"
+            else (lambda x: torch.from_numpy(x).cuda()))
+    tq, tk, tv, tdy = (conv(x) for x in feats)
+    plan = gt.Plan(sub_rp, sub_ci, h, d, dtype=cfg.dtype, scale=scale)
+    y, lse = plan.fwd(tq, tk, tv)
+    dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy)
+    torch.cuda.synchronize()
+    out = {}
+    for name, got, ref in zip(("y", "dq", "dk", "dv"), (y, dq, dk, dv), refs):
+        g = got.to(torch.float64).cpu().numpy()
+        den = float(np.max(np.abs(ref))) or 1.0
+        out[name] = float(np.max(np.abs(g - ref)) / den)
+    plan.close()
+    out["tol"] = 2e-2 if cfg.dtype == "bf16" else 1e-4
+    return out
 
 
 def cpu_sample_size(rp, ci, cfg, scale, budget_s):
@@ -355,10 +378,13 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         target = args.cpu_sample_edges or cpu_sample_size(rp, ci, cfg, scale, budget_s=15.0)
         sub_rp, sub_ci, R = induced_prefix_subgraph(rp, ci, target)
-        tc = oracle_step(sub_rp, sub_ci, R, cfg, 9, scale)
+        tc, feats, refs = oracle_step(sub_rp, sub_ci, R, cfg, 9, scale, keep=True)
         cpu = {"value": float(sub_rp[-1]) / tc, "unit": "edges/s", "cores": gtgen.num_threads(), "kind": "oracle",
                "sample": f"fp64 oracle fwd+bwd on the subgraph induced by the first {R} nodes "
-                         f"({int(sub_rp[-1])} entries), {tc:.1f} s"}
+                         f"({int(sub_rp[-1])} entries), {tc:.1f} s",
+               # the CUDA path on the same sample and inputs against these oracle results
+               "parity_normwise": sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs)}
+        del feats, refs
 
     if rank == 0:
         value = nnz / (ms * 1e-3)
