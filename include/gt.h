@@ -112,7 +112,11 @@ typedef struct {
   int partition;           /* 0 => rows+edges balanced (reading Z9), 1 => node-balanced */
   int device;              /* CUDA device ordinal; -1 => the calling thread's current device */
   int heavy_threshold;     /* rows/columns with more entries are split into chunks; 0 => 512 */
-  const char* beta_profile;/* optional path of a measured-beta JSON; NULL => probe at plan time */
+  const char* beta_profile;/* optional path of a measured-beta JSON (GT_AUTO): {"allgather": B,
+                              "halo": B, "a2a": B}, B = seconds per exchanged row, a number or an
+                              object keyed by the GPU count ({"2": .., "8": ..}, as written by
+                              paper_2604_16715_b200.agp); given strategies skip the plan-time probe.
+                              NULL => probe every candidate.  Unreadable file => GT_EINVAL. */
   int profile;             /* 1 => record CUDA events around every stage (gt_plan_timings) */
   int edge_state;          /* per-entry state of the backward (Table 1 keeps U per edge,
                               P:166): 0 => materialise when it fits in 85 % of free device memory,

@@ -123,6 +123,8 @@ def main():
     ap.add_argument("--sizes", default="65536,262144,1048576", help="node rows per collective (sweep)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--profile-out", default=None,
+                    help="write {collective: {GPU count: beta}} for gt_opts.beta_profile (Plan(beta_profile=...))")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -142,6 +144,10 @@ def main():
         if args.out:
             with open(args.out, "w") as f:
                 f.write(line + "\n")
+        if args.profile_out:
+            prof = {c: {str(p): float(beta[ci, p]) for p in range(2, P + 1)} for ci, c in enumerate(COLLECTIVES)}
+            with open(args.profile_out, "w") as f:
+                json.dump(prof, f)
     dist.destroy_process_group()
 
 

@@ -4,7 +4,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -143,6 +145,33 @@ static void make_ag_pattern(const gt_plan_s* P, Pattern& pt) {
 }
 
 static int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
+
+// Measured-beta profile (gt_opts.beta_profile; Fig. 2 / Alg. 3, reading Z14): a JSON object
+// {"allgather": B, "halo": B, "a2a": B} where B is seconds per exchanged row, either a number or an
+// object keyed by the GPU count ({"2": b2, "8": b8}, as written by paper_2604_16715_b200.agp).
+// Returns NaN for a strategy the file does not give (that candidate is probed instead).
+static double profile_beta(const std::string& text, const char* name, int world) {
+  const std::string key = std::string("\"") + name + "\"";
+  size_t at = text.find(key);
+  if (at == std::string::npos) return NAN;
+  at = text.find(':', at + key.size());
+  if (at == std::string::npos) return NAN;
+  ++at;
+  while (at < text.size() && std::isspace((unsigned char)text[at])) ++at;
+  if (at < text.size() && text[at] == '{') {  // per GPU count
+    const size_t end = text.find('}', at);
+    const std::string obj = text.substr(at, end == std::string::npos ? std::string::npos : end - at);
+    const std::string wk = "\"" + std::to_string(world) + "\"";
+    size_t w = obj.find(wk);
+    if (w == std::string::npos) return NAN;
+    w = obj.find(':', w + wk.size());
+    if (w == std::string::npos) return NAN;
+    return std::strtod(obj.c_str() + w + 1, nullptr);
+  }
+  char* endp = nullptr;
+  const double v = std::strtod(text.c_str() + at, &endp);
+  return endp == text.c_str() + at ? NAN : v;
+}
 
 // The forward pattern reversed, for the reduce-scatter backward: every received row (halo slot, or
 // padded all-gather block row) goes back to its owner as an fp32 partial.  send_idx of the result
@@ -550,6 +579,15 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     size_t free_b = 0, total_b = 0;
     GT_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
     const int64_t rs_bytes = 2 * D * 4;  // one fp32 partial dK || dV row (reduce-scatter backward)
+    std::string prof;
+    if (opts->beta_profile && opts->beta_profile[0]) {
+      FILE* fp = std::fopen(opts->beta_profile, "rb");
+      if (!fp) return fail(GT_EINVAL, std::string("gt_plan: cannot read beta_profile ") + opts->beta_profile);
+      char buf[4096];
+      size_t got;
+      while ((got = std::fread(buf, 1, sizeof(buf), fp)) > 0) prof.append(buf, got);
+      std::fclose(fp);
+    }
     for (int c : {(int)GT_ALLGATHER, (int)GT_HALO}) {
       const Pattern& f = c == GT_ALLGATHER ? pf_ag : pf_halo;
       const Pattern rev = P->bwd_reduce ? reverse_pattern(P.get(), f, c == GT_ALLGATHER) : Pattern();
@@ -564,7 +602,10 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       GT_TRY(P->comm->max_host(&misfit, st));  // every rank must agree (the probe below is collective)
       const double fits = misfit > 0 ? 0.0 : 1.0;
       double t_ex = INFINITY;
-      if (strategy == GT_AUTO && fits > 0) {
+      const double pb = prof.empty() ? NAN : profile_beta(prof, c == GT_ALLGATHER ? "allgather" : "halo", world);
+      if (strategy == GT_AUTO && fits > 0 && std::isfinite(pb)) {
+        t_ex = pb * (double)(f.recv_rows + b.recv_rows);  // profiled beta x rows moved (Eq. 7 term)
+      } else if (strategy == GT_AUTO && fits > 0) {
         // measure the forward and backward exchanges of this pattern (2 warm-up + 3 timed)
         DevBuf sb, rf, rb;
         int64_t sbytes = std::max({(int64_t)f.send_idx.size() * P->kv_row_bytes,
@@ -623,7 +664,14 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       double misfit = (double)need < 0.85 * (double)free_a ? 0.0 : 1.0;
       GT_TRY(P->comm->max_host(&misfit, st));
       if (misfit > 0 && strategy == GT_A2A) return fail(GT_ENOMEM, "gt_plan: GP-A2A buffers do not fit in device memory");
-      if (misfit == 0 && strategy == GT_AUTO) {
+      const double pa = prof.empty() ? NAN : profile_beta(prof, "a2a", world);
+      if (misfit == 0 && strategy == GT_AUTO && std::isfinite(pa)) {
+        const double t_ex = pa * 8.0 * (double)(n - P->n_local);
+        P->info.beta_s_per_row[GT_A2A] = pa;
+        P->info.predicted_ms[GT_A2A] = (t_iter1 / world + t_ex) * 1e3;
+        P->info.agp_score[GT_A2A] = world * t_ex / (world - 1) * 1e3;
+        P->info.agp_feasible[GT_A2A] = world * t_ex / (world - 1) <= t_iter1;
+      } else if (misfit == 0 && strategy == GT_AUTO) {
         std::vector<int64_t> loff(world), lcnt(world), goff(world), gcnt(world);
         for (int s = 0; s < world; ++s) {
           loff[s] = (int64_t)s * P->n_local;

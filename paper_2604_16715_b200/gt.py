@@ -269,13 +269,14 @@ class Plan:
     heavy_threshold (0 -> 512); partition 0 (rows + edges) | 1 (nodes); edge_state 0 | 1 | -1
     (materialised logits and (P, dP): auto / on / off); bwd_mode 0 (transposed owner) | 1
     (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); cuda_graphs (world-1 graph
-    replay); profile (per-stage CUDA events).
+    replay); beta_profile (JSON of measured beta per strategy for GT_AUTO instead of plan-time probes);
+    profile (per-stage CUDA events).
     """
 
     def __init__(self, row_ptr, col_idx, heads: int, d: int, dtype="bf16", scale: float = 0.0, world: int = 1,
                  rank: int = 0, comm=None, strategy="auto", heavy_threshold: int = 0, partition: int = 0,
                  validate: bool = True, device: int = -1, profile: bool = False, edge_state: int = 0,
-                 bwd_mode: int = 0, transport: int = 0, cuda_graphs: bool = False):
+                 bwd_mode: int = 0, transport: int = 0, cuda_graphs: bool = False, beta_profile=None):
         L = lib()
         self.row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         self.col_idx = np.ascontiguousarray(col_idx, np.int32)
@@ -296,6 +297,8 @@ class Plan:
         opts.bwd_mode = int(bwd_mode)
         opts.transport = int(transport)
         opts.cuda_graphs = int(cuda_graphs)
+        self._beta_profile = str(beta_profile).encode() if beta_profile else None  # kept alive for gt_plan
+        opts.beta_profile = self._beta_profile
         if world > 1:
             if isinstance(comm, LoopbackGroup):
                 opts.comm_kind, opts.comm = GT_COMM_LOOPBACK, comm.handle

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0, bwd_mode=0,
-                 transport=0, steps=1):
+                 transport=0, steps=1, beta_profile=None):
     import torch
     import paper_2604_16715_b200 as gt
     n = len(rp) - 1
@@ -36,7 +36,7 @@ def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=
             s = torch.cuda.Stream()
             plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, world=world, rank=r, comm=grp,
                            strategy=strategy, heavy_threshold=heavy, partition=partition, edge_state=edge_state,
-                           bwd_mode=bwd_mode, transport=transport)
+                           bwd_mode=bwd_mode, transport=transport, beta_profile=beta_profile)
             lo, hi = plan.row_lo, plan.row_hi
             with torch.cuda.stream(s):
                 tq, tk, tv, tdy = (t[lo:hi].contiguous() for t in full)
@@ -199,3 +199,17 @@ def test_peer_gather_config_errors():
         assert e.value.status == 3
     finally:
         grp.close()
+
+
+def test_auto_follows_a_beta_profile(tmp_path):
+    """gt_opts.beta_profile (Fig. 2 / Alg. 3 profiled beta, reading Z14) replaces the plan-time probe:
+    the planner's choice follows the profile, per GPU count or as plain numbers."""
+    import json
+    rp, ci = gtgen.random_graph(2000, 24000, seed=151, directed=True, power=2.1)
+    for fast, slow in (("allgather", "halo"), ("halo", "allgather")):
+        path = tmp_path / f"beta_{fast}.json"
+        path.write_text(json.dumps({fast: {"2": 1e-12, "3": 1e-12}, slow: 1.0, "a2a": 1.0}))
+        _, res = run_loopback(rp, ci, 4, 64, "f32", 2, "auto", seed=1510, beta_profile=str(path))
+        assert {r[4]["strategy_name"] for r in res} == {fast}
+        for r in res:
+            assert r[4]["beta_s_per_row"][{"allgather": 2, "halo": 3}[fast]] == pytest.approx(1e-12)
