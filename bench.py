@@ -35,11 +35,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--strategy", default=None, help="auto|allgather|halo (world > 1)")
+    ap.add_argument("--strategy", default=None, help="auto|allgather|halo|a2a (world > 1)")
     ap.add_argument("--heavy", type=int, default=int(os.environ.get("GT_HEAVY", "0")),
                     help="heavy row/column threshold (0 = library default)")
     ap.add_argument("--edge-state", type=int, default=int(os.environ.get("GT_EDGE_STATE", "0")),
                     help="gt_opts.edge_state: 0 auto (materialise when it fits), 1 on, -1 recompute")
+    ap.add_argument("--transport", type=int, default=int(os.environ.get("GT_TRANSPORT", "0")),
+                    help="gt_opts.transport (world > 1): 0 copies, 1 fused peer gather over NVLink")
     ap.add_argument("--bwd-mode", type=int, default=0,
                     help="gt_opts.bwd_mode (world > 1): 0 transposed owner, 1 reduce-scatter of fp32 partials")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -276,7 +278,7 @@ def run_ours(args):
     t_plan = time.perf_counter()
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
                    strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local,
-                   edge_state=args.edge_state, bwd_mode=args.bwd_mode)
+                   edge_state=args.edge_state, bwd_mode=args.bwd_mode, transport=args.transport)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     info = plan.info()
@@ -398,7 +400,7 @@ def run_ours(args):
                              "no flush",
                        "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 512,
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
-                       "bwd_mode": info["bwd_mode"]},
+                       "bwd_mode": info["bwd_mode"], "transport": info["transport"]},
             "roofline": roofline,
             "step_hbm_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
             "stages_ms": {s: stages[s][0] / max(stages[s][1], 1) for s in stages},
