@@ -372,6 +372,14 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
   static_assert(!((ES & 1) && PASS == 2 && HALO), "the ES column pass reads local rows only");
   using C = PC<T, H, D, PASS, ES>;
   constexpr int EPL = C::EPL, LPH = C::LPH, RB = C::RB, EB = C::EB, U = C::U, LB = C::LB;
+#ifndef GT_FWD_BFLY
+#define GT_FWD_BFLY 1
+#endif
+  constexpr bool kBfly = GT_FWD_BFLY && PASS == 0 && LPH == 8 && U == 4;  // forward butterfly (see below)
+#ifndef GT_ROWB_BFLY
+#define GT_ROWB_BFLY 1
+#endif
+  constexpr bool kBflyR = GT_ROWB_BFLY && PASS == 1 && (ES & 2) && LPH == 8 && U == 4;  // row-pass butterfly
   extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -613,7 +621,54 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         }
       }
       const int cnt = cur.cnt;
-      if constexpr (PASS == 0) {
+      if constexpr (PASS == 0 && kBfly) {
+        // Transposed (reduce-scatter) butterfly over the head's 8 lanes: the 4 per-lane partial dot
+        // products of the stage are summed so that lane group g = 2 b2 + b1 (b = lane bits) ends up
+        // with neighbour g's full score (14 instructions instead of 4 x 6); max and exp are then taken
+        // once per lane, and the 4 weights broadcast back for the SpMM.  l is kept per lane group and
+        // summed over the groups at the end of the row.
+        float part[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t kw[W];
+          lds_raw<W>(st + u * EB + lane * LB, kw);
+          part[u] = dot_raw<T, W>(ow, kw);
+        }
+        const bool b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+        float a0 = b2 ? part[2] : part[0], a1 = b2 ? part[3] : part[1];
+        const float t0 = b2 ? part[0] : part[2], t1 = b2 ? part[1] : part[3];
+        a0 += __shfl_xor_sync(kFull, t0, 4);
+        a1 += __shfl_xor_sync(kFull, t1, 4);
+        float r = b1 ? a1 : a0;
+        r += __shfl_xor_sync(kFull, b1 ? a0 : a1, 2);
+        r += __shfl_xor_sync(kFull, r, 1);
+        const int ug = 2 * (int)b2 + (int)b1;  // this lane's neighbour
+        const float sv = r * a.qscale;
+        const float sl = ug < cnt ? sv : -INFINITY;
+        if constexpr (ES & 2) {  // s2[entry e0 + u][head] for the row pass: one coalesced store per stage
+          reinterpret_cast<float*>(xs + s * C::XS)[ug * H + head] = sv;  // lanes b0 = 0, 1 agree
+          __syncwarp();
+          const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
+          st_pred(a.es_out + (int64_t)cur.e0 * H + lane, x[lane < U * H ? lane : 0], lane < cnt * H);
+        }
+        float mx = fmaxf(sl, __shfl_xor_sync(kFull, sl, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
+        mx = fmaxf(mx, m);
+        const float corr = ex2(m - mx);
+        l *= corr;
+        scale2<EPL>(corr, acc);
+        const float pl = ex2(sl - mx);  // 0 for masked neighbours
+        l += pl;
+        const int base = lane & ~7;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float p = __shfl_sync(kFull, pl, base | ((u >> 1) << 2) | ((u & 1) << 1));
+          float vf[EPL];
+          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
+          axpy<EPL>(p, vf, acc);
+        }
+        m = mx;
+      } else if constexpr (PASS == 0) {
         float sc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -643,6 +698,54 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           axpy<EPL>(p, vf, acc);
         }
         m = mx;
+      } else if constexpr (PASS == 1 && kBflyR) {
+        // Row pass with stored logits: the 4 partial dP = <dY_i, v_j> are reduced by the same transposed
+        // butterfly (lane group g = 2 b2 + b1 ends with neighbour g's dP); p is computed once per lane for
+        // its neighbour, (p, dP) stored, and (p, p dP) broadcast back for the two SpMM accumulators.
+        float part[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t vw[W];
+          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+          part[u] = dot_raw<T, W>(ow, vw);
+        }
+        const bool b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+        float a0 = b2 ? part[2] : part[0], a1 = b2 ? part[3] : part[1];
+        const float t0 = b2 ? part[0] : part[2], t1 = b2 ? part[1] : part[3];
+        a0 += __shfl_xor_sync(kFull, t0, 4);
+        a1 += __shfl_xor_sync(kFull, t1, 4);
+        float dpl = b1 ? a1 : a0;
+        dpl += __shfl_xor_sync(kFull, b1 ? a0 : a1, 2);
+        dpl += __shfl_xor_sync(kFull, dpl, 1);
+        const int ug = 2 * (int)b2 + (int)b1;
+        const float s_ = reinterpret_cast<const float*>(st + U * EB)[ug * H + head];  // forward's logit
+        const float pl = ug < cnt ? ex2(s_ - m) : 0.f;
+        const float pdl = pl * dpl;
+        l += pdl;  // per lane group; summed over the groups at the end of the row
+        if constexpr (ES & 1)  // lanes b0 = 0, 1 write the same 8 bytes
+          reinterpret_cast<float2*>(xs + s * C::XS)[ug * H + head] = make_float2(pl, dpl);
+        const int base = lane & ~7;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int src = base | ((u >> 1) << 2) | ((u & 1) << 1);
+          const float p = __shfl_sync(kFull, pl, src);
+          const float pd = __shfl_sync(kFull, pdl, src);
+          float kf[EPL];
+          lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
+          axpy<EPL>(pd, kf, acc);
+          axpy<EPL>(p, kf, acc2);
+        }
+        if constexpr (ES & 1) {
+          __syncwarp();
+          const float2* x = reinterpret_cast<const float2*>(xs + s * C::XS);
+          // (same per-stage store as the generic row pass below)
+          const float* xf = reinterpret_cast<const float*>(x);
+#pragma unroll
+          for (int t = 0; t < (2 * U * H + 31) / 32; ++t) {
+            const int f = lane + 32 * t;
+            st_pred(a.es_out + (int64_t)cur.e0 * (2 * H) + f, xf[f < 2 * U * H ? f : 0], f < 2 * cnt * H);
+          }
+        }
       } else if constexpr (PASS == 1) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -700,12 +803,20 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         const int32_t own = cur.own;
         if (own < 0) {  // chunk of a heavy row/column: partial state for the merge kernel
           const int64_t ch = -1 - (int64_t)own;
+          if constexpr (PASS == 0 && kBfly) {  // l per lane group -> the row's (chunk's) l
+            l += __shfl_xor_sync(kFull, l, 2);
+            l += __shfl_xor_sync(kFull, l, 4);
+          }
           if constexpr (PASS == 0) {
             float* pp = a.part + ch * (int64_t)(D + 2 * H);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
             { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
           } else if constexpr (PASS == 1) {
+            if constexpr (kBflyR) {
+              l += __shfl_xor_sync(kFull, l, 2);
+              l += __shfl_xor_sync(kFull, l, 4);
+            }
             float* pp = a.part + ch * (int64_t)(2 * D + H);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
@@ -717,6 +828,10 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           }
         } else {
           const int64_t r = own;
+          if constexpr (PASS == 0 && kBfly) {
+            l += __shfl_xor_sync(kFull, l, 2);
+            l += __shfl_xor_sync(kFull, l, 4);
+          }
           if constexpr (PASS == 0) {
             const float inv = 1.f / l;
 #pragma unroll
@@ -724,6 +839,10 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
             a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
           } else if constexpr (PASS == 1) {
+            if constexpr (kBflyR) {
+              l += __shfl_xor_sync(kFull, l, 2);
+              l += __shfl_xor_sync(kFull, l, 4);
+            }
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] = a.scale * fmaf(-l, acc2[i], acc[i]);
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
