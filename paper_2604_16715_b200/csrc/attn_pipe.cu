@@ -348,6 +348,40 @@ __device__ __forceinline__ float head_sum(float x) {
   return x;
 }
 
+// Transposed (reduce-scatter) butterfly of 4 per-lane partial sums over a head's LPH lanes (LPH >= 4):
+// the two top lane bits of the head pick the neighbour, g = 2 b_top + b_top-1, whose full sum the lane
+// ends with (the lower levels are plain xor-sums).  bfly_src(u) is a lane holding neighbour u's sum.
+template <int LPH>
+struct Bfly {
+  static constexpr int TOP = LPH == 32 ? 4 : (LPH == 16 ? 3 : (LPH == 8 ? 2 : 1));
+  static_assert(LPH >= 4 && (1 << (TOP + 1)) == LPH, "butterfly needs 4..32 lanes per head");
+  static __device__ __forceinline__ int group(int lane) { return 2 * ((lane >> TOP) & 1) + ((lane >> (TOP - 1)) & 1); }
+  static __device__ __forceinline__ int src(int lane, int u) {
+    return (lane & ~(LPH - 1)) | ((u >> 1) << TOP) | ((u & 1) << (TOP - 1));
+  }
+  static __device__ __forceinline__ float reduce(const float (&v)[4], int lane) {
+    const bool bh = (lane >> TOP) & 1, bl = (lane >> (TOP - 1)) & 1;
+    float a0 = bh ? v[2] : v[0], a1 = bh ? v[3] : v[1];
+    const float t0 = bh ? v[0] : v[2], t1 = bh ? v[1] : v[3];
+    a0 += __shfl_xor_sync(0xffffffffu, t0, 1 << TOP);
+    a1 += __shfl_xor_sync(0xffffffffu, t1, 1 << TOP);
+    float r = bl ? a1 : a0;
+    r += __shfl_xor_sync(0xffffffffu, bl ? a0 : a1, 1 << (TOP - 1));
+#pragma unroll
+    for (int o = (1 << (TOP - 1)) >> 1; o >= 1; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+  }
+  // sum (or max) over the 4 neighbour groups of a per-group value
+  static __device__ __forceinline__ float all_sum(float x) {
+    x += __shfl_xor_sync(0xffffffffu, x, 1 << (TOP - 1));
+    return x + __shfl_xor_sync(0xffffffffu, x, 1 << TOP);
+  }
+  static __device__ __forceinline__ float all_max(float x) {
+    x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1 << (TOP - 1)));
+    return fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1 << TOP));
+  }
+};
+
 struct Meta {      // warp-uniform description of one filled stage
   int32_t e0;      // entry index (in `nbr` order) of the stage's first neighbour (nnz < 2^31)
   int32_t own;     // row/column id, or chunk -1 - c
@@ -375,11 +409,11 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #ifndef GT_FWD_BFLY
 #define GT_FWD_BFLY 1
 #endif
-  constexpr bool kBfly = GT_FWD_BFLY && PASS == 0 && LPH == 8 && U == 4;  // forward butterfly (see below)
+  constexpr bool kBfly = GT_FWD_BFLY && PASS == 0 && LPH >= 4 && U == 4;  // forward butterfly (see below)
 #ifndef GT_ROWB_BFLY
 #define GT_ROWB_BFLY 1
 #endif
-  constexpr bool kBflyR = GT_ROWB_BFLY && PASS == 1 && (ES & 2) && LPH == 8 && U == 4;  // row-pass butterfly
+  constexpr bool kBflyR = GT_ROWB_BFLY && PASS == 1 && (ES & 2) && LPH >= 4 && U == 4;  // row-pass butterfly
   extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -622,11 +656,11 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       }
       const int cnt = cur.cnt;
       if constexpr (PASS == 0 && kBfly) {
-        // Transposed (reduce-scatter) butterfly over the head's 8 lanes: the 4 per-lane partial dot
-        // products of the stage are summed so that lane group g = 2 b2 + b1 (b = lane bits) ends up
-        // with neighbour g's full score (14 instructions instead of 4 x 6); max and exp are then taken
-        // once per lane, and the 4 weights broadcast back for the SpMM.  l is kept per lane group and
-        // summed over the groups at the end of the row.
+        // Transposed (reduce-scatter) butterfly over the head's lanes (Bfly): the 4 per-lane partial dot
+        // products of the stage are summed so that each lane group ends up with one neighbour's full
+        // score (14 instructions instead of 4 x 6 at 8 lanes per head); max and exp are then taken once
+        // per lane, and the 4 weights broadcast back for the SpMM.  l is kept per lane group and summed
+        // over the groups at the end of the row.
         float part[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -634,15 +668,9 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           lds_raw<W>(st + u * EB + lane * LB, kw);
           part[u] = dot_raw<T, W>(ow, kw);
         }
-        const bool b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
-        float a0 = b2 ? part[2] : part[0], a1 = b2 ? part[3] : part[1];
-        const float t0 = b2 ? part[0] : part[2], t1 = b2 ? part[1] : part[3];
-        a0 += __shfl_xor_sync(kFull, t0, 4);
-        a1 += __shfl_xor_sync(kFull, t1, 4);
-        float r = b1 ? a1 : a0;
-        r += __shfl_xor_sync(kFull, b1 ? a0 : a1, 2);
-        r += __shfl_xor_sync(kFull, r, 1);
-        const int ug = 2 * (int)b2 + (int)b1;  // this lane's neighbour
+        using B = Bfly<LPH>;
+        const float r = B::reduce(part, lane);
+        const int ug = B::group(lane);  // this lane's neighbour
         const float sv = r * a.qscale;
         const float sl = ug < cnt ? sv : -INFINITY;
         if constexpr (ES & 2) {  // s2[entry e0 + u][head] for the row pass: one coalesced store per stage
@@ -651,18 +679,15 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
           st_pred(a.es_out + (int64_t)cur.e0 * H + lane, x[lane < U * H ? lane : 0], lane < cnt * H);
         }
-        float mx = fmaxf(sl, __shfl_xor_sync(kFull, sl, 2));
-        mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, 4));
-        mx = fmaxf(mx, m);
+        const float mx = fmaxf(B::all_max(sl), m);
         const float corr = ex2(m - mx);
         l *= corr;
         scale2<EPL>(corr, acc);
         const float pl = ex2(sl - mx);  // 0 for masked neighbours
         l += pl;
-        const int base = lane & ~7;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float p = __shfl_sync(kFull, pl, base | ((u >> 1) << 2) | ((u & 1) << 1));
+          const float p = __shfl_sync(kFull, pl, B::src(lane, u));
           float vf[EPL];
           lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
           axpy<EPL>(p, vf, acc);
@@ -700,7 +725,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         m = mx;
       } else if constexpr (PASS == 1 && kBflyR) {
         // Row pass with stored logits: the 4 partial dP = <dY_i, v_j> are reduced by the same transposed
-        // butterfly (lane group g = 2 b2 + b1 ends with neighbour g's dP); p is computed once per lane for
+        // butterfly (each lane group ends with one neighbour's dP); p is computed once per lane for
         // its neighbour, (p, dP) stored, and (p, p dP) broadcast back for the two SpMM accumulators.
         float part[4];
 #pragma unroll
@@ -709,25 +734,18 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           lds_raw<W>(st + u * EB + RB + lane * LB, vw);
           part[u] = dot_raw<T, W>(ow, vw);
         }
-        const bool b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
-        float a0 = b2 ? part[2] : part[0], a1 = b2 ? part[3] : part[1];
-        const float t0 = b2 ? part[0] : part[2], t1 = b2 ? part[1] : part[3];
-        a0 += __shfl_xor_sync(kFull, t0, 4);
-        a1 += __shfl_xor_sync(kFull, t1, 4);
-        float dpl = b1 ? a1 : a0;
-        dpl += __shfl_xor_sync(kFull, b1 ? a0 : a1, 2);
-        dpl += __shfl_xor_sync(kFull, dpl, 1);
-        const int ug = 2 * (int)b2 + (int)b1;
+        using B = Bfly<LPH>;
+        const float dpl = B::reduce(part, lane);
+        const int ug = B::group(lane);
         const float s_ = reinterpret_cast<const float*>(st + U * EB)[ug * H + head];  // forward's logit
         const float pl = ug < cnt ? ex2(s_ - m) : 0.f;
         const float pdl = pl * dpl;
         l += pdl;  // per lane group; summed over the groups at the end of the row
         if constexpr (ES & 1)  // lanes b0 = 0, 1 write the same 8 bytes
           reinterpret_cast<float2*>(xs + s * C::XS)[ug * H + head] = make_float2(pl, dpl);
-        const int base = lane & ~7;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int src = base | ((u >> 1) << 2) | ((u & 1) << 1);
+          const int src = B::src(lane, u);
           const float p = __shfl_sync(kFull, pl, src);
           const float pd = __shfl_sync(kFull, pdl, src);
           float kf[EPL];
@@ -803,20 +821,14 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         const int32_t own = cur.own;
         if (own < 0) {  // chunk of a heavy row/column: partial state for the merge kernel
           const int64_t ch = -1 - (int64_t)own;
-          if constexpr (PASS == 0 && kBfly) {  // l per lane group -> the row's (chunk's) l
-            l += __shfl_xor_sync(kFull, l, 2);
-            l += __shfl_xor_sync(kFull, l, 4);
-          }
+          if constexpr (PASS == 0 && kBfly) l = Bfly<LPH>::all_sum(l);  // per lane group -> the row's (chunk's) l
           if constexpr (PASS == 0) {
             float* pp = a.part + ch * (int64_t)(D + 2 * H);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
             { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
           } else if constexpr (PASS == 1) {
-            if constexpr (kBflyR) {
-              l += __shfl_xor_sync(kFull, l, 2);
-              l += __shfl_xor_sync(kFull, l, 4);
-            }
+            if constexpr (kBflyR) l = Bfly<LPH>::all_sum(l);
             float* pp = a.part + ch * (int64_t)(2 * D + H);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
@@ -828,10 +840,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           }
         } else {
           const int64_t r = own;
-          if constexpr (PASS == 0 && kBfly) {
-            l += __shfl_xor_sync(kFull, l, 2);
-            l += __shfl_xor_sync(kFull, l, 4);
-          }
+          if constexpr (PASS == 0 && kBfly) l = Bfly<LPH>::all_sum(l);
           if constexpr (PASS == 0) {
             const float inv = 1.f / l;
 #pragma unroll
@@ -839,10 +848,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
             a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
           } else if constexpr (PASS == 1) {
-            if constexpr (kBflyR) {
-              l += __shfl_xor_sync(kFull, l, 2);
-              l += __shfl_xor_sync(kFull, l, 4);
-            }
+            if constexpr (kBflyR) l = Bfly<LPH>::all_sum(l);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] = a.scale * fmaf(-l, acc2[i], acc[i]);
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
