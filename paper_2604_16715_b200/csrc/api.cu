@@ -56,6 +56,7 @@ static gt_status upload_work(WorkList& w) {
   GT_TRY(upload(w.d_beg, w.beg.data(), w.beg.size()));
   GT_TRY(upload(w.d_end, w.end.data(), w.end.size()));
   GT_TRY(upload(w.d_own, w.own.data(), w.own.size()));
+  GT_TRY(upload(w.d_empty, w.empty.data(), w.empty.size()));
   GT_TRY(w.d_counter.alloc(sizeof(unsigned long long)));
   return GT_OK;
 }

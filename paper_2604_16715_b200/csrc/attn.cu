@@ -291,19 +291,24 @@ bool shape_supported(int heads, int d, int dtype) {
   return D == 64 || D == 128 || D == 256 || D == 512;
 }
 
+static int fills(const WorkList& w) { return w.empty.empty() ? 0 : 1; }
+
 int launches_fwd(const gt_plan_s* P) {
   if (P->fwd_split)
-    return (P->w_fwd[0].n > 0 ? 1 : 0) + (P->w_fwd[1].n > 0 ? 1 : 0) + (P->fwd_chunks.nchunks() > 0 ? 1 : 0);
-  return (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
+    return (P->w_fwd[0].n > 0 ? 1 : 0) + (P->w_fwd[1].n > 0 ? 1 : 0) + (P->fwd_chunks.nchunks() > 0 ? 1 : 0) +
+           fills(P->w_fwd[0]);
+  return (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0) + fills(P->w_rows);
 }
 int launches_bwd(const gt_plan_s* P) {
-  const int rows = (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0);
+  const int rows = (P->w_rows.n > 0 ? 1 : 0) + (P->heavy_rows.nchunks() > 0 ? 1 : 0) + fills(P->w_rows);
   if (P->bwd_reduce)
     return rows + (P->w_hcols.n > 0 ? 1 : 0) + (P->n_slots > 0 ? 1 : 0) + (P->w_colrs.n > 0 ? 1 : 0) +
+           fills(P->w_colrs) +
            (P->rs_chunks.ids.empty() ? 0 : 1);
   if (P->col_split)
-    return rows + (P->w_colp[0].n > 0 ? 1 : 0) + (P->w_colp[1].n > 0 ? 1 : 0) + (P->col_chunks.nchunks() > 0 ? 1 : 0);
-  return rows + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_cols.nchunks() > 0 ? 1 : 0);
+    return rows + (P->w_colp[0].n > 0 ? 1 : 0) + (P->w_colp[1].n > 0 ? 1 : 0) + (P->col_chunks.nchunks() > 0 ? 1 : 0) +
+           fills(P->w_colp[0]);
+  return rows + (P->w_cols.n > 0 ? 1 : 0) + (P->heavy_cols.nchunks() > 0 ? 1 : 0) + fills(P->w_cols);
 }
 
 // Entry-state arguments of a pass (Table 1 keeps Z and U per edge): the forward

@@ -867,6 +867,39 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
   }
 }
 
+// Outputs of rows (columns) without entries (reading Z4): Y = 0 and LSE = -inf (pass 0); dQ = 0 and
+// (LSE2, D) = (-inf, 0) (pass 1); dK = dV = 0 (pass 2).  One warp per id, grid-stride.
+template <int PASS>
+__global__ void __launch_bounds__(256) fill_empty_kernel(const int32_t* ids, int64_t n, char* out_a, char* out_b,
+                                                         float* out_f, int64_t rb, int heads, int sb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n; x += nw) {
+    const int64_t r = ids[x];
+    for (int64_t c = lane * 16; c < rb; c += 32 * 16) {
+      *reinterpret_cast<uint4*>(out_a + r * rb + c) = make_uint4(0, 0, 0, 0);
+      if constexpr (PASS == 2) *reinterpret_cast<uint4*>(out_b + r * rb + c) = make_uint4(0, 0, 0, 0);
+    }
+    if constexpr (PASS == 0) {
+      if (lane < heads) out_f[r * heads + lane] = -INFINITY;
+    } else if constexpr (PASS == 1) {
+      if (lane < heads)
+        reinterpret_cast<float2*>(reinterpret_cast<char*>(out_f) + r * sb)[lane] = make_float2(-INFINITY, 0.f);
+    }
+  }
+}
+
+gt_status fill_empty(int pass, const int32_t* ids, int64_t n, char* out_a, char* out_b, float* out_f, int64_t rb,
+                     int heads, int sb, cudaStream_t st) {
+  if (n <= 0) return GT_OK;
+  const int blocks = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 8);
+  if (pass == 0) fill_empty_kernel<0><<<blocks, 256, 0, st>>>(ids, n, out_a, out_b, out_f, rb, heads, sb);
+  else if (pass == 1) fill_empty_kernel<1><<<blocks, 256, 0, st>>>(ids, n, out_a, out_b, out_f, rb, heads, sb);
+  else fill_empty_kernel<2><<<blocks, 256, 0, st>>>(ids, n, out_a, out_b, out_f, rb, heads, sb);
+  GT_CUDA_TRY(cudaGetLastError());
+  return GT_OK;
+}
+
 // ----------------------------------------------------------------- launcher --
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
 gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
@@ -989,6 +1022,10 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.es_out = es.out;
   a.es_in = es.in;
   a.src = es.src;
+  if (!w.empty.empty())
+    GT_TRY(pipe::fill_empty(pass, w.d_empty.as<int32_t>(), (int64_t)w.empty.size(), (char*)out_a, (char*)out_b,
+                            out_f, (int64_t)P->heads * P->d * (P->dtype == GT_F32 ? 4 : 2), P->heads,
+                            (int)P->st_row_bytes, st));
   return pipe::dispatch(P->dtype, P->heads, P->heads * P->d, pass, a, st, reserve_sms);
 }
 

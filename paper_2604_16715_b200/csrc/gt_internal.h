@@ -93,6 +93,10 @@ struct WorkList {
   std::vector<int32_t> own;
   DevBuf d_beg, d_end, d_own, d_counter;
   int64_t n = 0;
+  // rows (columns) without entries are not work items (one atomicAdd each would dominate graphs
+  // with many of them, e.g. R-MAT's 56 %): a streaming kernel writes their outputs
+  std::vector<int32_t> empty;
+  DevBuf d_empty;
 };
 
 // One segment of a row's entries assigned to a phase (0 or 1) of a split pass.

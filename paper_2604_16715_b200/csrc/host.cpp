@@ -139,7 +139,7 @@ void build_work(int64_t count, const std::function<void(int64_t, std::vector<Seg
                 int nphase, WorkList* phases, ChunkTable* t, const std::function<bool(int64_t)>& force) {
   t->ids.clear(); t->first.clear(); t->chunk_lo.clear(); t->chunk_hi.clear(); t->chunk_owner.clear();
   for (int ph = 0; ph < nphase; ++ph) {
-    phases[ph].beg.clear(); phases[ph].end.clear(); phases[ph].own.clear();
+    phases[ph].beg.clear(); phases[ph].end.clear(); phases[ph].own.clear(); phases[ph].empty.clear();
   }
   std::vector<Segment> sg, pieces;
   for (int64_t r = 0; r < count; ++r) {
@@ -164,7 +164,8 @@ void build_work(int64_t count, const std::function<void(int64_t, std::vector<Seg
       }
     } else if (pieces.empty()) {
       const int64_t at = sg.empty() ? 0 : sg.front().lo;
-      phases[0].beg.push_back(at); phases[0].end.push_back(at); phases[0].own.push_back((int32_t)r);
+      (void)at;
+      phases[0].empty.push_back((int32_t)r);
     } else if (pieces.size() == 1) {
       WorkList& w = phases[pieces[0].phase];
       w.beg.push_back(pieces[0].lo); w.end.push_back(pieces[0].hi); w.own.push_back((int32_t)r);
