@@ -21,7 +21,7 @@
 // holding up to U neighbours (two feature rows, plus the neighbour's (LSE2, D) pair in pass 2, plus
 // the stage's entry state), and an "own" slot per stage for the data of the row (column) an item
 // starts.  Warps grab kG consecutive work items (rows, or chunks of heavy rows, in row order) per
-// atomicAdd (kG = 1, A/B-tuned), so the resident warps sweep the graph in a narrow window of rows and
+// atomicAdd (kG = 2, A/B-tuned on C3 and C5), so the resident warps sweep the graph in a narrow window of rows and
 // the neighbours they gather stay in L2 (community locality); consecutive items have contiguous
 // entry ranges, streamed through a 32-entry register window of neighbour ids with the next window
 // prefetched.  Rows with more than the plan's threshold of entries are split into chunks whose fp32
@@ -57,7 +57,7 @@ constexpr unsigned kFull = 0xffffffffu;
 #define GT_PIPE_STAGES 2
 #endif
 #ifndef GT_PIPE_GRAB
-#define GT_PIPE_GRAB 1
+#define GT_PIPE_GRAB 2
 #endif
 constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
 constexpr int kS = GT_PIPE_STAGES;      // stages per warp (2 measured best: more resident warps)
