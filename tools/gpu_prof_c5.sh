@@ -8,3 +8,4 @@ for i in 0 1 2; do
   python tools/ncu_summary.py /tmp/c5_pass$i.ncu-rep > gpurun_out/c5_ncu_pass$i.txt 2>&1
 done
 echo done
+timeout 900 python bench.py --config C5 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/c5_bench.log 2>&1
