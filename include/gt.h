@@ -174,6 +174,9 @@ typedef struct {
   int64_t edge_state_bytes;       /* device bytes of that state */
   int bwd_mode;                   /* backward dataflow in use (gt_opts.bwd_mode; 0 when world == 1) */
   int transport;                  /* forward K || V transport in use (gt_opts.transport) */
+  int64_t fwd_gen;                /* gt_attn_fwd calls made on this plan */
+  int64_t stale_bwds;             /* gt_attn_bwd calls whose (q, k, v, lse) were not those of the last
+                                     gt_attn_fwd (they re-fetched / recomputed the forward's state) */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,
@@ -220,8 +223,13 @@ gt_status gt_attn_fwd(gt_plan_t plan, const void* q, const void* k, const void* 
  * [n_local, heads, d] upstream gradient.  dq, dk, dv: device [n_local, heads, d] outputs (same
  * dtype, round-to-nearest-even from fp32 accumulation).  Collective when world > 1.
  * The plan retains state of the LAST gt_attn_fwd it ran (the received K||V rows when world > 1, the
- * per-entry logits with edge_state, the head slices with GT_A2A): gt_attn_bwd uses it and returns
- * GT_ESTATE when no gt_attn_fwd has run on this plan and such state is needed. */
+ * per-entry logits with edge_state, the head slices with GT_A2A), tagged with that forward's
+ * (q, k, v, lse) pointers.  gt_attn_bwd uses the state only when its own (q, k, v, lse) are those
+ * tensors; otherwise (another forward ran in between, e.g. several layers sharing one plan, or no
+ * forward ran at all) it re-fetches the K||V rows / head slices for these k, v and recomputes the
+ * logits from q, k — correct for any call order, at the cost of the extra exchange and dot products
+ * (gt_plan_info.stale_bwds counts such calls).  With world > 1 every rank must see the same match,
+ * which holds when all ranks make the same sequence of calls on live tensors. */
 gt_status gt_attn_bwd(gt_plan_t plan, const void* q, const void* k, const void* v, const float* lse,
                       const void* dy, void* dq, void* dk, void* dv, void* stream);
 

@@ -945,6 +945,8 @@ gt_status gt_plan(const gt_csr* csr, int64_t n, int64_t nnz, int heads, int d, i
 gt_status gt_plan_info_get(gt_plan_t P, gt_plan_info* out) {
   if (!P || !out) return fail(GT_EINVAL, "gt_plan_info_get: null argument");
   *out = P->info;
+  out->fwd_gen = (int64_t)P->fwd_gen;
+  out->stale_bwds = P->stale_bwds;
   return GT_OK;
 }
 
@@ -1017,6 +1019,40 @@ static gt_status check_ptrs(gt_plan_t P, std::initializer_list<const void*> ps) 
   return GT_OK;
 }
 
+// K||V rows of the forward halo (pack + all-gather / all-to-all-v) on the side stream, ordered after the
+// work already on `st`; ev_halo marks their arrival.  Collective.
+static gt_status fwd_exchange(gt_plan_t P, const void* k, const void* v, cudaStream_t st) {
+  const int elt = P->dtype == GT_F32 ? 4 : 2;
+  const int64_t D = (int64_t)P->heads * P->d;
+  cudaEvent_t ev2 = nullptr;
+  GT_CUDA_TRY(cudaEventRecord(P->ev_fwd0, st));
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_fwd0, 0));
+  P->mark_begin(0, P->side, &ev2);
+  GT_TRY(pack_kv(k, v, P->d_send_out_idx.as<int32_t>(), P->n_send_out, D, elt, P->d_send_buf.p, P->side));
+  if (P->strategy == GT_ALLGATHER)
+    GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_kv.p, P->n_max, P->kv_row_bytes, P->side));
+  else
+    GT_TRY(P->comm->exchange(P->d_send_buf.p, P->so_off.data(), P->so_cnt.data(), P->d_recv_kv.p, P->ro_off.data(),
+                             P->ro_cnt.data(), P->kv_row_bytes, P->side));
+  P->mark_end(0, P->side, ev2);
+  GT_CUDA_TRY(cudaEventRecord(P->ev_halo, P->side));
+  return GT_OK;
+}
+
+static void set_fwd_tag(gt_plan_t P, const void* q, const void* k, const void* v, const void* lse) {
+  P->fwd_tag[0] = q;
+  P->fwd_tag[1] = k;
+  P->fwd_tag[2] = v;
+  P->fwd_tag[3] = lse;
+  P->fwd_gen++;
+  P->fwd_done = true;
+}
+
+// True when the plan's retained forward state belongs to the forward of these tensors.
+static bool fwd_fresh(gt_plan_t P, const void* q, const void* k, const void* v, const void* lse) {
+  return P->fwd_done && P->fwd_tag[0] == q && P->fwd_tag[1] == k && P->fwd_tag[2] == v && P->fwd_tag[3] == lse;
+}
+
 static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse,
                                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -1035,51 +1071,49 @@ static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const
     GT_TRY(a2a_gather(P, P->d_hy.p, gb, P->d_stage[0].p, y, st));
     GT_TRY(a2a_gather(P, P->d_hlse.p, lb, P->d_stage[1].p, lse, st));
     P->mark_end(0, st, e1);
-    P->fwd_done = true;
+    set_fwd_tag(P, q, k, v, lse);
     return GT_OK;
   }
   const void* halo = nullptr;
-  cudaEvent_t ev = nullptr, ev2 = nullptr;
+  cudaEvent_t ev = nullptr;
   if (P->peer) {  // fused peer gather: no exchange, the kernels read remote rows from the owners
     P->mark_begin(1, st, &ev);
     GT_TRY(launch_fwd_peer(P, q, k, v, y, lse, st));
     P->mark_end(1, st, ev);
-    P->fwd_done = true;
+    set_fwd_tag(P, q, k, v, lse);
     return GT_OK;
   }
   if (P->world > 1) {
     // K||V rows of the halo on the side stream, overlapped with phase A (owned-column entries)
-    const int elt = P->dtype == GT_F32 ? 4 : 2;
-    const int64_t D = (int64_t)P->heads * P->d;
-    GT_CUDA_TRY(cudaEventRecord(P->ev_fwd0, st));
-    GT_CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_fwd0, 0));
-    P->mark_begin(0, P->side, &ev2);
-    GT_TRY(pack_kv(k, v, P->d_send_out_idx.as<int32_t>(), P->n_send_out, D, elt, P->d_send_buf.p, P->side));
-    if (P->strategy == GT_ALLGATHER)
-      GT_TRY(P->comm->all_gather(P->d_send_buf.p, P->d_recv_kv.p, P->n_max, P->kv_row_bytes, P->side));
-    else
-      GT_TRY(P->comm->exchange(P->d_send_buf.p, P->so_off.data(), P->so_cnt.data(), P->d_recv_kv.p,
-                               P->ro_off.data(), P->ro_cnt.data(), P->kv_row_bytes, P->side));
-    P->mark_end(0, P->side, ev2);
-    GT_CUDA_TRY(cudaEventRecord(P->ev_halo, P->side));
+    GT_TRY(fwd_exchange(P, k, v, st));
     halo = P->d_recv_kv.p;
   }
   P->mark_begin(1, st, &ev);
   GT_TRY(launch_fwd(P, q, k, v, halo, y, lse, st, P->world > 1 ? P->ev_halo : nullptr));
   P->mark_end(1, st, ev);
-  P->fwd_done = true;
+  set_fwd_tag(P, q, k, v, lse);
   return GT_OK;
 }
 
+// fresh: the retained forward state belongs to this backward's (q, k, v, lse) (fwd_fresh).  A stale
+// backward re-fetches what the forward fetched (K||V halo rows, published rows, head slices) and
+// recomputes the logits instead of reading the stored ones.
 static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse,
-                                const void* dy, void* dq, void* dk, void* dv, void* stream) {
+                                const void* dy, void* dq, void* dk, void* dv, void* stream, bool fresh) {
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
+  if (!fresh) P->stale_bwds++;
   if (P->strategy == GT_A2A) {  // GP-A2A: scatter dY and LSE, all rows for this rank's heads, gather grads
     const int64_t gb = (int64_t)P->heads_l * P->d * (P->dtype == GT_F32 ? 4 : 2);
     const int64_t lb = (int64_t)P->heads_l * 4;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     P->mark_begin(3, st, &e0);
+    if (!fresh) {  // the head slices of q, k, v belong to another forward: scatter these
+      GT_TRY(a2a_scatter(P, q, gb, P->d_stage[0].p, P->d_hq.p, st));
+      GT_TRY(a2a_scatter(P, k, gb, P->d_stage[1].p, P->d_hk.p, st));
+      GT_TRY(a2a_scatter(P, v, gb, P->d_stage[2].p, P->d_hv.p, st));
+      P->sub->fwd_done = false;  // and so do the sub-plan's stored logits
+    }
     GT_TRY(a2a_scatter(P, dy, gb, P->d_stage[0].p, P->d_hdy.p, st));
     GT_TRY(a2a_scatter(P, lse, lb, P->d_stage[1].p, P->d_hlse.p, st));
     P->mark_end(3, st, e0);
@@ -1097,12 +1131,22 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   const bool multi = P->world > 1;
   const bool ag = P->strategy == GT_ALLGATHER;
+  if (multi && !fresh) {
+    if (P->peer) {  // publish these k, v once every peer is done with the rows published before
+      const int elt = P->dtype == GT_F32 ? 4 : 2;
+      GT_TRY(P->comm->stream_barrier(st));
+      GT_TRY(pack_kv(k, v, P->d_iota.as<int32_t>(), P->n_local, (int64_t)P->heads * P->d, elt, P->d_pub.p, st));
+    } else {        // the forward's exchange again, for these k, v
+      GT_TRY(fwd_exchange(P, k, v, st));
+      GT_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_halo, 0));
+    }
+  }
   if (multi && P->bwd_reduce) {
     // Reduce-scatter backward (reading Z11): row pass; fp32 partials of the halo columns, sent to their
     // owners on the side stream while the owned columns run; then the fixed-order merge.
     P->mark_begin(2, st, &ev);
-    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
-    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecord(P->ev_dq_ready, st));
+    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st, fresh));
+    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecordWithFlags(P->ev_dq_ready, st, cudaEventRecordExternal));
     GT_TRY(launch_bwd_halo_cols(P, q, dy, st));
     P->mark_end(2, st, ev);
     GT_CUDA_TRY(cudaEventRecord(P->ev_rows, st));
@@ -1126,8 +1170,8 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     P->mark_begin(2, st, &ev);
     GT_TRY(P->comm->stream_barrier(st));
     GT_TRY(pack_kv(q, dy, P->d_iota.as<int32_t>(), P->n_local, (int64_t)P->heads * P->d, elt, P->d_pub_qd.p, st));
-    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
-    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecord(P->ev_dq_ready, st));
+    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st, fresh));
+    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecordWithFlags(P->ev_dq_ready, st, cudaEventRecordExternal));
     P->mark_end(2, st, ev);
     P->mark_begin(4, st, &ev);
     GT_TRY(launch_bwd_cols_peer(P, q, k, v, dy, dk, dv, st));
@@ -1151,8 +1195,8 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     P->mark_end(3, P->side, ev2);
   }
   P->mark_begin(2, st, &ev);
-  GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st));
-  if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecord(P->ev_dq_ready, st));
+  GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st, fresh));
+  if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecordWithFlags(P->ev_dq_ready, st, cudaEventRecordExternal));
   P->mark_end(2, st, ev);
   if (multi) {
     // (LSE2, D) blocks of the in-halo rows: written by the row pass on their owners
@@ -1226,7 +1270,7 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
     GT_CUDA_TRY(cudaSetDevice(P->device));
     const gt_plan_s::GraphKey key = {q, k, v, y, lse, nullptr, nullptr, nullptr, nullptr, nullptr};
     GT_TRY(graph_run(P, P->gfwd, key, st, [&] { return attn_fwd_eager(P, q, k, v, y, lse, stream); }));
-    P->fwd_done = true;
+    set_fwd_tag(P, q, k, v, lse);
     return GT_OK;
   }
   GT_TRY(attn_fwd_eager(P, q, k, v, y, lse, stream));
@@ -1237,17 +1281,15 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
 gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse, const void* dy,
                       void* dq, void* dk, void* dv, void* stream) {
   GT_TRY(check_ptrs(P, {q, k, v, lse, dy, dq, dk, dv}));
-  if ((P->world > 1 || P->es_logits) && !P->fwd_done)
-    return fail(GT_ESTATE, "gt_attn_bwd before gt_attn_fwd: the plan uses the forward's retained state "
-                           "(received K||V rows, per-entry logits or GP-A2A head slices)");
+  const bool fresh = fwd_fresh(P, q, k, v, lse);
   cudaStream_t st = (cudaStream_t)stream;
   if (graph_ok(P, st, P->bwd_warm)) {
     GT_CUDA_TRY(cudaSetDevice(P->device));
-    const gt_plan_s::GraphKey key = {q, k, v, lse, dy, dq, dk, dv, P->ev_dq_ready, nullptr};
+    const gt_plan_s::GraphKey key = {q, k, v, lse, dy, dq, dk, dv, P->ev_dq_ready, fresh ? (const void*)1 : nullptr};
     return graph_run(P, P->gbwd, key, st,
-                     [&] { return attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream); });
+                     [&] { return attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream, fresh); });
   }
-  GT_TRY(attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream));
+  GT_TRY(attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream, fresh));
   P->bwd_warm = true;
   return GT_OK;
 }

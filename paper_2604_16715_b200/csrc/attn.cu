@@ -212,13 +212,10 @@ __global__ void __launch_bounds__(kBlock) colb_merge_list_kernel(int64_t nids, c
 
 template <typename K>
 int merge_grid(K, int64_t ids) {  // one warp per heavy row, at most 4 blocks per SM (tiny kernels)
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int64_t cap = (int64_t)sms * 4;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);  // per call: plans may use several devices
+  const int64_t cap = (int64_t)std::max(sms, 1) * 4;
   return (int)std::max<int64_t>(1, std::min<int64_t>(cap, (ids * 32 + kBlock - 1) / kBlock));
 }
 
@@ -314,13 +311,13 @@ int launches_bwd(const gt_plan_s* P) {
 // Entry-state arguments of a pass (Table 1 keeps Z and U per edge): the forward
 // stores base-2 logits and the row pass (P, dP) per entry in local CSR order; the row pass reads the
 // logits in the same order, the column pass reads (P, dP) through the CSC -> CSR map.
-static EntryState entry_state(gt_plan_s* P, int pass) {
+static EntryState entry_state(gt_plan_s* P, int pass, bool use_logits = true) {
   EntryState e;
   if (!P->es) return e;
   if (pass == 0) {
     if (P->es_logits) e.out = P->d_s2.as<float>();
   } else if (pass == 1) {
-    if (P->es_logits) e.in = P->d_s2.as<float>();
+    if (P->es_logits && use_logits) e.in = P->d_s2.as<float>();
     e.out = P->d_pd.as<float>();
   } else if (pass == 2) {
     e.in = P->d_pd.as<float>();
@@ -408,9 +405,9 @@ gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void
 }
 
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
-                          const float* lse, const void* dy, void* dq, cudaStream_t st) {
+                          const float* lse, const void* dy, void* dq, cudaStream_t st, bool use_logits) {
   GT_TRY(pipe_pass(P, 1, P->w_rows, P->heavy_rows, P->d_part_rowb.as<float>(), q, dy, lse, k, v, halo_kv, nullptr,
-                   dq, nullptr, P->d_stats.as<float>(), st, 0, entry_state(P, 1)));
+                   dq, nullptr, P->d_stats.as<float>(), st, 0, entry_state(P, 1, use_logits)));
   if (P->heavy_rows.nchunks() > 0) {
     MergeArgs m = merge_args(P->heavy_rows, P->d_part_rowb, P->scale);
     m.dq = (char*)dq;

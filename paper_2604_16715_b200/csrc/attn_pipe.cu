@@ -40,6 +40,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "gt_internal.h"
@@ -50,6 +51,7 @@ namespace pipe {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxDevices = 64;
 #ifndef GT_PIPE_WARPS
 #define GT_PIPE_WARPS 4
 #endif
@@ -904,28 +906,34 @@ gt_status fill_empty(int pass, const int32_t* ids, int64_t n, char* out_a, char*
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
 gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
   using C = PC<T, H, D, PASS, ES>;
-  static int grid = 0;
+  // per device (the smem attribute and the SM count are per device; plans may live on several)
+  static std::mutex mu;
+  static int grid_of[kMaxDevices] = {}, sms_of[kMaxDevices] = {};
   const size_t smem = (size_t)kWarps * C::WARP_SMEM;
-  if (!grid) {
-    auto k = pipe_kernel<T, H, D, PASS, HALO, ES>;
-    GT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    GT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, smem));
-    if (const char* cap = std::getenv("GT_CTAS_PER_SM"))  // tuning: narrower in-flight window of rows
-      per = std::min(per, std::max(1, std::atoi(cap)));
-    grid = sms * std::max(per, 1);
+  int dev = 0;
+  GT_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(GT_ECONFIG, "device ordinal out of range");
+  int grid = 0, sms = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!grid_of[dev]) {
+      auto k = pipe_kernel<T, H, D, PASS, HALO, ES>;
+      GT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per = 0;
+      GT_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
+      GT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, smem));
+      if (const char* cap = std::getenv("GT_CTAS_PER_SM"))  // tuning: narrower in-flight window of rows
+        per = std::min(per, std::max(1, std::atoi(cap)));
+      grid_of[dev] = sms_of[dev] * std::max(per, 1);
+    }
+    grid = grid_of[dev];
+    sms = sms_of[dev];
   }
   if (a.nitems <= 0) return GT_OK;
   const int64_t want = (a.nitems + kG - 1) / kG;
   int cap = grid;
-  if (reserve_sms > 0) {  // leave SMs free for concurrent communication kernels (overlap phases)
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (reserve_sms > 0)  // leave SMs free for concurrent communication kernels (overlap phases)
     cap = std::max(1, grid - grid / sms * reserve_sms);
-  }
   const int g = (int)std::min<int64_t>(cap, (want + kWarps - 1) / kWarps);
   GT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
   pipe_kernel<T, H, D, PASS, HALO, ES><<<g, kWarps * 32, smem, st>>>(a);

@@ -192,6 +192,13 @@ struct gt_plan_s {
   int64_t in_row_bytes = 0;                               // kv + st: bytes per backward-halo row
   cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr, ev_fwd0 = nullptr, ev_halo = nullptr;
   bool fwd_done = false;
+  // Which forward the retained state (received / published K||V rows, per-entry logits, GP-A2A head
+  // slices) belongs to: the (q, k, v, lse) pointers of the last gt_attn_fwd and its sequence number.
+  // gt_attn_bwd uses the state only when its own (q, k, v, lse) are the same tensors; otherwise it
+  // re-fetches the K||V rows / head slices and recomputes the logits (a stale backward).
+  const void* fwd_tag[4] = {};
+  uint64_t fwd_gen = 0;
+  int64_t stale_bwds = 0;          // backward calls that could not use the retained state
 
   // fused peer-gather transport (opts.transport = 1): every rank publishes its K || V
   // rows in d_pub; the forward's remote-column entries and the row pass read remote rows straight from
@@ -257,8 +264,10 @@ gt_status launch_bwd_cols_peer(gt_plan_s* P, const void* q, const void* k, const
 // forward with the fused peer-gather transport
 gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void* v, void* y, float* lse,
                           cudaStream_t st);
+// use_logits: read the forward's stored logits (false: recompute q.k; the stored ones belong to
+// another forward)
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
-                          const float* lse, const void* dy, void* dq, cudaStream_t st);
+                          const float* lse, const void* dy, void* dq, cudaStream_t st, bool use_logits = true);
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
                           const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st,
                           cudaEvent_t side_ready);

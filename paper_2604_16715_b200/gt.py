@@ -56,7 +56,7 @@ class _Info(ctypes.Structure):
                    ("agp_score", ctypes.c_double * 5), ("agp_feasible", ctypes.c_int * 5),
                    ("alpha_s_per_unit", ctypes.c_double), ("edge_state", ctypes.c_int),
                    ("edge_state_bytes", ctypes.c_int64), ("bwd_mode", ctypes.c_int),
-                   ("transport", ctypes.c_int)])
+                   ("transport", ctypes.c_int), ("fwd_gen", ctypes.c_int64), ("stale_bwds", ctypes.c_int64)])
 
 
 _lib = None
@@ -311,6 +311,10 @@ class Plan:
         _check(L.gt_plan(ctypes.byref(csr), n, nnz, heads, d, world, ctypes.byref(opts), ctypes.byref(h)))
         self.handle = h.value
         self.heads, self.d, self.dtype_code = heads, d, opts.dtype
+        self.device = int(device)
+        if self.device < 0:
+            import torch
+            self.device = torch.cuda.current_device() if torch.cuda.is_available() else 0
         inf = self.info()
         self.n_local = inf["n_local"]
         self.row_lo, self.row_hi = inf["row_lo"], inf["row_hi"]
@@ -350,14 +354,25 @@ class Plan:
         import torch
         return torch.float32 if self.dtype_code == GT_F32 else torch.bfloat16
 
-    def _check_tensor(self, t, name):
+    def _check_tensor(self, t, name, lse=False):
+        """Shape, dtype, layout and device of a tensor passed to the C ABI (which sees only pointers):
+        feature tensors are [n_local, heads, d] of the plan dtype, lse is float32 [n_local, heads],
+        all contiguous and on the plan's device.  Raises GTError(GT_EINVAL) (SPEC.md S:56, S:66
+        "shape error") instead of letting a kernel read or write out of bounds."""
         import torch
         if not isinstance(t, torch.Tensor) or not t.is_cuda:
-            raise ValueError(f"{name} must be a CUDA tensor")
-        if t.dtype != self._torch_dtype() and name != "lse":
-            raise ValueError(f"{name}: dtype {t.dtype} != plan dtype {self._torch_dtype()}")
+            raise GTError(GT_EINVAL, f"{name} must be a CUDA tensor")
+        want_dt = torch.float32 if lse else self._torch_dtype()
+        want_shape = (self.n_local, self.heads) if lse else (self.n_local, self.heads, self.d)
+        if t.dtype != want_dt:
+            raise GTError(GT_EINVAL, f"{name}: dtype {t.dtype} != {want_dt}")
+        if tuple(t.shape) != want_shape:
+            raise GTError(GT_EINVAL, f"{name}: shape {tuple(t.shape)} != {want_shape} (n_local, heads"
+                                     f"{'' if lse else ', d'})")
         if not t.is_contiguous():
-            raise ValueError(f"{name} must be contiguous")
+            raise GTError(GT_EINVAL, f"{name} must be contiguous")
+        if t.device.index != self.device:
+            raise GTError(GT_EINVAL, f"{name} is on cuda:{t.device.index}, the plan on cuda:{self.device}")
 
     @staticmethod
     def _stream(stream):
@@ -369,10 +384,10 @@ class Plan:
         import torch
         for t, nm in ((q, "q"), (k, "k"), (v, "v")):
             self._check_tensor(t, nm)
-        if y is None:
-            y = torch.empty_like(q)
-        if lse is None:
-            lse = torch.empty((q.shape[0], self.heads), dtype=torch.float32, device=q.device)
+        y = torch.empty_like(q) if y is None else y
+        lse = torch.empty((self.n_local, self.heads), dtype=torch.float32, device=q.device) if lse is None else lse
+        self._check_tensor(y, "y")
+        self._check_tensor(lse, "lse", lse=True)
         _check(lib().gt_attn_fwd(self.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), y.data_ptr(),
                                  lse.data_ptr(), self._stream(stream)))
         return y, lse
@@ -381,15 +396,28 @@ class Plan:
         import torch
         for t, nm in ((q, "q"), (k, "k"), (v, "v"), (dy, "dy")):
             self._check_tensor(t, nm)
+        self._check_tensor(lse, "lse", lse=True)
         dq = torch.empty_like(q) if dq is None else dq
         dk = torch.empty_like(k) if dk is None else dk
         dv = torch.empty_like(v) if dv is None else dv
+        for t, nm in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+            self._check_tensor(t, nm)
         _check(lib().gt_attn_bwd(self.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), lse.data_ptr(),
                                  dy.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), self._stream(stream)))
         return dq, dk, dv
 
     def fwd_bwd_host(self, q, k, v, dy, y, lse, dq, dk, dv, stream=None):
         """End-to-end step through the C-ABI with host buffers (pinned CPU tensors)."""
+        import torch
+        for t, nm in ((q, "q"), (k, "k"), (v, "v"), (dy, "dy"), (y, "y"), (lse, "lse"), (dq, "dq"), (dk, "dk"),
+                      (dv, "dv")):
+            if t is None and nm not in ("q", "k", "v", "dy"):
+                continue
+            want_dt = torch.float32 if nm == "lse" else self._torch_dtype()
+            want = (self.n_local, self.heads) if nm == "lse" else (self.n_local, self.heads, self.d)
+            if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != want_dt or tuple(t.shape) != want \
+                    or not t.is_contiguous():
+                raise GTError(GT_EINVAL, f"{nm}: expected a contiguous host tensor {want_dt} {want}")
         ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         _check(lib().gt_attn_fwd_bwd_host(self.handle, ptr(q), ptr(k), ptr(v), ptr(dy), ptr(y), ptr(lse),
                                           ptr(dq), ptr(dk), ptr(dv), self._stream(stream)))

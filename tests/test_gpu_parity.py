@@ -180,13 +180,30 @@ def test_errors_are_reported(gt):
     with pytest.raises(gt.GTError) as e:
         gt.Plan(rp, ci, 4, 64, edge_state=2)
     assert e.value.status == 1  # GT_EINVAL
-    # backward before any forward on a plan with entry-state logits: the retained state is missing
+    # shape / dtype / device errors of the binding: GT_EINVAL, no kernel launched
     import torch
     plan = gt.Plan(rp, ci, 4, 64, dtype="f32", edge_state=1)
     z = torch.zeros((4, 4, 64), dtype=torch.float32, device="cuda")
-    with pytest.raises(gt.GTError) as e:
-        plan.bwd(z, z, z, torch.zeros((4, 4), dtype=torch.float32, device="cuda"), z)
-    assert e.value.status == 7  # GT_ESTATE
+    lz = torch.zeros((4, 4), dtype=torch.float32, device="cuda")
+    bad_cases = [
+        lambda: plan.fwd(torch.zeros((3, 4, 64), device="cuda"), z, z),                # n_local
+        lambda: plan.fwd(z, torch.zeros((4, 2, 128), device="cuda"), z),               # heads, d
+        lambda: plan.fwd(z, z, z.to(torch.bfloat16)),                                  # dtype
+        lambda: plan.fwd(z, z, torch.zeros((4, 64, 4), device="cuda").transpose(1, 2)),  # layout
+        lambda: plan.fwd(z, z, z, y=torch.zeros((2, 4, 64), device="cuda")),            # output shape
+        lambda: plan.fwd(z, z, z, lse=torch.zeros((4, 4), dtype=torch.float64, device="cuda")),
+        lambda: plan.bwd(z, z, z, torch.zeros((4, 3), device="cuda"), z),              # lse shape
+        lambda: plan.bwd(z, z, z, lz.to(torch.bfloat16), z),                           # lse dtype
+        lambda: plan.bwd(z, z, z, lz, z, dq=torch.zeros((5, 4, 64), device="cuda")),   # output shape
+        lambda: plan.bwd(z.cpu(), z, z, lz, z),                                        # device
+    ]
+    for i, f in enumerate(bad_cases):
+        with pytest.raises(gt.GTError) as e:
+            f()
+        assert e.value.status == 1, i  # GT_EINVAL
+    # a backward with no forward before it is no longer an error: it recomputes (test_gpu_state_binding)
+    plan.bwd(z, z, z, lz, z)
+    torch.cuda.synchronize()
     plan.close()
 
 
