@@ -190,7 +190,7 @@ def sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs):
     tq, tk, tv, tdy = (conv(x) for x in feats)
     plan = gt.Plan(sub_rp, sub_ci, h, d, dtype=cfg.dtype, scale=scale)
     y, lse = plan.fwd(tq, tk, tv)
-    dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy)
+    dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
     torch.cuda.synchronize()
     out = {}
     for name, got, ref in zip(("y", "dq", "dk", "dv"), (y, dq, dk, dv), refs):
@@ -299,7 +299,7 @@ def run_ours(args):
 
     def step():
         plan.fwd(q, k, v, y, lse)
-        plan.bwd(q, k, v, lse, dy, dq, dk, dv)
+        plan.bwd(q, k, v, y, lse, dy, dq, dk, dv)
 
     for _ in range(max(args.warmup, 0)):
         step()

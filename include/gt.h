@@ -219,9 +219,13 @@ gt_status gt_plan_export(gt_plan_t plan, int what, int peer, void* dst, int64_t 
 gt_status gt_attn_fwd(gt_plan_t plan, const void* q, const void* k, const void* v, void* y, float* lse,
                       void* stream);
 
-/* Backward.  q, k, v, lse as passed to / produced by the matching gt_attn_fwd; dy: device
+/* Backward.  q, k, v, y, lse as passed to / produced by the matching gt_attn_fwd; dy: device
  * [n_local, heads, d] upstream gradient.  dq, dk, dv: device [n_local, heads, d] outputs (same
  * dtype, round-to-nearest-even from fp32 accumulation).  Collective when world > 1.
+ * D_i = sum_e U_e dP_e is taken as <dY_i, Y_i> (equal, since sum_e U_e = 1), so the
+ * row pass knows it before its first entry; dS_e = U_e (dP_e - D_i).  With bf16 tensors the weights
+ * U_e, dS_e of the SpMM products are rounded to bf16 (the products are exact in fp32 and accumulated
+ * in fp32), as the PV and dS K products of FlashAttention are (reading Z23).
  * The plan retains state of the LAST gt_attn_fwd it ran (the received K||V rows when world > 1, the
  * per-entry logits with edge_state, the head slices with GT_A2A), tagged with that forward's
  * (q, k, v, lse) pointers.  gt_attn_bwd uses the state only when its own (q, k, v, lse) are those
@@ -230,7 +234,7 @@ gt_status gt_attn_fwd(gt_plan_t plan, const void* q, const void* k, const void* 
  * logits from q, k — correct for any call order, at the cost of the extra exchange and dot products
  * (gt_plan_info.stale_bwds counts such calls).  With world > 1 every rank must see the same match,
  * which holds when all ranks make the same sequence of calls on live tensors. */
-gt_status gt_attn_bwd(gt_plan_t plan, const void* q, const void* k, const void* v, const float* lse,
+gt_status gt_attn_bwd(gt_plan_t plan, const void* q, const void* k, const void* v, const void* y, const float* lse,
                       const void* dy, void* dq, void* dk, void* dv, void* stream);
 
 /* End-to-end step with HOST buffers (pinned for full speed): copies q, k, v, dy host->device,

@@ -862,7 +862,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     if (opts->edge_state >= 0) {
       const char* lg = std::getenv("GT_ES_LOGITS");  // logits half of the state (A/B switch; default on)
       const bool logits = !(lg && lg[0] == '0');
-      const int64_t es_bytes = P->nnz_local * heads * (logits ? 12 : 8) + P->nnz_in_local * 4;
+      // per entry and head: the logit (f32) and (P, dS) (bf16x2 for bf16 plans, f32x2 for f32 plans)
+      const int64_t pdb = P->dtype == GT_F32 ? 8 : 4;
+      const int64_t es_bytes = P->nnz_local * heads * ((logits ? 4 : 0) + pdb) + P->nnz_in_local * 4;
       size_t free_b = 0, total_b = 0;
       GT_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
       double misfit = (double)es_bytes < 0.85 * (double)free_b ? 0.0 : 1.0;
@@ -874,7 +876,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     }
     if (P->es) {
       if (P->es_logits) GT_TRY(P->d_s2.alloc(std::max<size_t>((size_t)P->nnz_local, 1) * heads * sizeof(float)));
-      GT_TRY(P->d_pd.alloc(std::max<size_t>((size_t)P->nnz_local, 1) * heads * 2 * sizeof(float)));
+      GT_TRY(P->d_pd.alloc(std::max<size_t>((size_t)P->nnz_local, 1) * heads * (P->dtype == GT_F32 ? 8 : 4)));
       GT_TRY(P->d_src.alloc(std::max<size_t>((size_t)P->nnz_in_local, 1) * sizeof(int32_t)));
       GT_TRY(build_local_src(full_src.as<int32_t>(), c0, c1, csr->row_ptr[P->lo], csr->row_ptr[P->hi],
                              P->d_src.as<int32_t>(), st));
@@ -915,7 +917,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   const int64_t nrc = P->heavy_rows.nchunks(), ncc = P->col_split ? P->col_chunks.nchunks() : P->heavy_cols.nchunks();
   const int64_t nfc = P->fwd_split ? P->fwd_chunks.nchunks() : nrc;
   GT_TRY(P->d_part_fwd.alloc((size_t)std::max<int64_t>(nfc, 1) * (D + 2 * heads) * sizeof(float)));
-  GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * (2 * D + heads) * sizeof(float)));
+  GT_TRY(P->d_part_rowb.alloc((size_t)std::max<int64_t>(nrc, 1) * D * sizeof(float)));
   GT_TRY(P->d_part_colb.alloc((size_t)std::max<int64_t>(ncc, 1) * (2 * D) * sizeof(float)));
   GT_TRY(P->d_stats.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->stats_stride * sizeof(float)));
   if (P->peer) GT_TRY(P->comm->share_pointers(P->d_stats.p, P->peer_st, st));  // read by the peers' column pass
@@ -1048,6 +1050,16 @@ static void set_fwd_tag(gt_plan_t P, const void* q, const void* k, const void* v
   P->fwd_done = true;
 }
 
+// Records `ev` on `st`; under stream capture as an external event node, so that replaying the graph
+// records it again (a plain record inside a capture only orders the captured work).
+static gt_status record_external(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  GT_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive) GT_CUDA_TRY(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+  else GT_CUDA_TRY(cudaEventRecord(ev, st));
+  return GT_OK;
+}
+
 // True when the plan's retained forward state belongs to the forward of these tensors.
 static bool fwd_fresh(gt_plan_t P, const void* q, const void* k, const void* v, const void* lse) {
   return P->fwd_done && P->fwd_tag[0] == q && P->fwd_tag[1] == k && P->fwd_tag[2] == v && P->fwd_tag[3] == lse;
@@ -1098,8 +1110,9 @@ static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const
 // fresh: the retained forward state belongs to this backward's (q, k, v, lse) (fwd_fresh).  A stale
 // backward re-fetches what the forward fetched (K||V halo rows, published rows, head slices) and
 // recomputes the logits instead of reading the stored ones.
-static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse,
-                                const void* dy, void* dq, void* dk, void* dv, void* stream, bool fresh) {
+static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, const void* y,
+                                const float* lse, const void* dy, void* dq, void* dk, void* dv, void* stream,
+                                bool fresh) {
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
   if (!fresh) P->stale_bwds++;
@@ -1115,10 +1128,11 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
       P->sub->fwd_done = false;  // and so do the sub-plan's stored logits
     }
     GT_TRY(a2a_scatter(P, dy, gb, P->d_stage[0].p, P->d_hdy.p, st));
+    GT_TRY(a2a_scatter(P, y, gb, P->d_stage[2].p, P->d_hy.p, st));
     GT_TRY(a2a_scatter(P, lse, lb, P->d_stage[1].p, P->d_hlse.p, st));
     P->mark_end(3, st, e0);
-    GT_TRY(gt_attn_bwd(P->sub, P->d_hq.p, P->d_hk.p, P->d_hv.p, P->d_hlse.as<float>(), P->d_hdy.p, P->d_hdq.p,
-                       P->d_hdk.p, P->d_hdv.p, stream));
+    GT_TRY(gt_attn_bwd(P->sub, P->d_hq.p, P->d_hk.p, P->d_hv.p, P->d_hy.p, P->d_hlse.as<float>(), P->d_hdy.p,
+                       P->d_hdq.p, P->d_hdk.p, P->d_hdv.p, stream));
     P->mark_begin(3, st, &e1);
     GT_TRY(a2a_gather(P, P->d_hdq.p, gb, P->d_stage[0].p, dq, st));
     GT_TRY(a2a_gather(P, P->d_hdk.p, gb, P->d_stage[1].p, dk, st));
@@ -1145,8 +1159,8 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     // Reduce-scatter backward (reading Z11): row pass; fp32 partials of the halo columns, sent to their
     // owners on the side stream while the owned columns run; then the fixed-order merge.
     P->mark_begin(2, st, &ev);
-    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st, fresh));
-    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecordWithFlags(P->ev_dq_ready, st, cudaEventRecordExternal));
+    GT_TRY(launch_bwd_rows(P, q, k, v, y, halo_kv, lse, dy, dq, st, fresh));
+    if (P->ev_dq_ready) GT_TRY(record_external(P->ev_dq_ready, st));
     GT_TRY(launch_bwd_halo_cols(P, q, dy, st));
     P->mark_end(2, st, ev);
     GT_CUDA_TRY(cudaEventRecord(P->ev_rows, st));
@@ -1170,8 +1184,8 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     P->mark_begin(2, st, &ev);
     GT_TRY(P->comm->stream_barrier(st));
     GT_TRY(pack_kv(q, dy, P->d_iota.as<int32_t>(), P->n_local, (int64_t)P->heads * P->d, elt, P->d_pub_qd.p, st));
-    GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st, fresh));
-    if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecordWithFlags(P->ev_dq_ready, st, cudaEventRecordExternal));
+    GT_TRY(launch_bwd_rows(P, q, k, v, y, halo_kv, lse, dy, dq, st, fresh));
+    if (P->ev_dq_ready) GT_TRY(record_external(P->ev_dq_ready, st));
     P->mark_end(2, st, ev);
     P->mark_begin(4, st, &ev);
     GT_TRY(launch_bwd_cols_peer(P, q, k, v, dy, dk, dv, st));
@@ -1195,8 +1209,8 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     P->mark_end(3, P->side, ev2);
   }
   P->mark_begin(2, st, &ev);
-  GT_TRY(launch_bwd_rows(P, q, k, v, halo_kv, lse, dy, dq, st, fresh));
-  if (P->ev_dq_ready) GT_CUDA_TRY(cudaEventRecordWithFlags(P->ev_dq_ready, st, cudaEventRecordExternal));
+  GT_TRY(launch_bwd_rows(P, q, k, v, y, halo_kv, lse, dy, dq, st, fresh));
+  if (P->ev_dq_ready) GT_TRY(record_external(P->ev_dq_ready, st));
   P->mark_end(2, st, ev);
   if (multi) {
     // (LSE2, D) blocks of the in-halo rows: written by the row pass on their owners
@@ -1268,7 +1282,7 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   cudaStream_t st = (cudaStream_t)stream;
   if (graph_ok(P, st, P->fwd_warm)) {
     GT_CUDA_TRY(cudaSetDevice(P->device));
-    const gt_plan_s::GraphKey key = {q, k, v, y, lse, nullptr, nullptr, nullptr, nullptr, nullptr};
+    const gt_plan_s::GraphKey key = {q, k, v, y, lse, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     GT_TRY(graph_run(P, P->gfwd, key, st, [&] { return attn_fwd_eager(P, q, k, v, y, lse, stream); }));
     set_fwd_tag(P, q, k, v, lse);
     return GT_OK;
@@ -1278,18 +1292,19 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   return GT_OK;
 }
 
-gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const float* lse, const void* dy,
-                      void* dq, void* dk, void* dv, void* stream) {
-  GT_TRY(check_ptrs(P, {q, k, v, lse, dy, dq, dk, dv}));
+gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const void* y, const float* lse,
+                      const void* dy, void* dq, void* dk, void* dv, void* stream) {
+  GT_TRY(check_ptrs(P, {q, k, v, y, lse, dy, dq, dk, dv}));
   const bool fresh = fwd_fresh(P, q, k, v, lse);
   cudaStream_t st = (cudaStream_t)stream;
   if (graph_ok(P, st, P->bwd_warm)) {
     GT_CUDA_TRY(cudaSetDevice(P->device));
-    const gt_plan_s::GraphKey key = {q, k, v, lse, dy, dq, dk, dv, P->ev_dq_ready, fresh ? (const void*)1 : nullptr};
+    const gt_plan_s::GraphKey key = {q, k, v, y, lse, dy, dq, dk, dv, P->ev_dq_ready,
+                                     fresh ? (const void*)1 : nullptr};
     return graph_run(P, P->gbwd, key, st,
-                     [&] { return attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream, fresh); });
+                     [&] { return attn_bwd_eager(P, q, k, v, y, lse, dy, dq, dk, dv, stream, fresh); });
   }
-  GT_TRY(attn_bwd_eager(P, q, k, v, lse, dy, dq, dk, dv, stream, fresh));
+  GT_TRY(attn_bwd_eager(P, q, k, v, y, lse, dy, dq, dk, dv, stream, fresh));
   P->bwd_warm = true;
   return GT_OK;
 }
@@ -1332,8 +1347,8 @@ gt_status gt_attn_fwd_bwd_host(gt_plan_t P, const void* q, const void* k, const 
   GT_CUDA_TRY(cudaEventRecord(ev_fwd, st));
   GT_CUDA_TRY(cudaStreamWaitEvent(st, ev_dy, 0));
   P->ev_dq_ready = P->ev_dq;
-  gt_status bs = gt_attn_bwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[5].as<float>(), P->h2d[3].p,
-                             P->h2d[6].p, P->h2d[7].p, P->h2d[8].p, stream);
+  gt_status bs = gt_attn_bwd(P, P->h2d[0].p, P->h2d[1].p, P->h2d[2].p, P->h2d[4].p, P->h2d[5].as<float>(),
+                             P->h2d[3].p, P->h2d[6].p, P->h2d[7].p, P->h2d[8].p, stream);
   P->ev_dq_ready = nullptr;
   GT_TRY(bs);
   if (P->strategy == GT_A2A) GT_CUDA_TRY(cudaEventRecord(P->ev_dq, st));  // dQ arrives with dK, dV there

@@ -6,7 +6,7 @@
 // merge kernels below combine them in chunk order (deterministic, no atomics):
 //   forward   (m_c, l_c, acc_c):  M = max m_c, L = sum l_c 2^(m_c - M), y = sum acc_c 2^(m_c - M) / L,
 //                                 LSE = (M + log2 L) ln 2          (log-sum-exp merge of online softmax)
-//   row pass  (A_c, C_c, D_c):    dQ = scale (sum A_c - (sum D_c)(sum C_c)),  D = sum D_c
+//   row pass  A_c = sum dS k:     dQ = scale sum A_c   (D_i = <dY_i, Y_i> is known to every chunk)
 //   col pass  (dK_c, dV_c):       dK = scale sum dK_c,  dV = sum dV_c
 // (The first-round register-gather kernels are superseded by attn_pipe.cu; their measurements are
 // in profiles/r01 and DESIGN.md.)
@@ -112,24 +112,17 @@ __global__ void __launch_bounds__(kBlock) rowb_merge_kernel(MergeArgs a) {
   for (int64_t x = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < a.nids; x += nw) {
     const int64_t row = a.ids[x];
     const int c0 = a.first[x], c1 = a.first[x + 1];
-    float A[EPL], Cc[EPL], Ds = 0.f;
+    float A[EPL];
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) { A[i] = 0.f; Cc[i] = 0.f; }
+    for (int i = 0; i < EPL; ++i) A[i] = 0.f;
     for (int c = c0; c < c1; ++c) {
-      const float* pp = a.part + (int64_t)c * (2 * D + H);
+      const float* pp = a.part + (int64_t)c * D;
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) {
-        A[i] += pp[lane * EPL + i];
-        Cc[i] += pp[D + lane * EPL + i];
-      }
-      Ds += pp[2 * D + head];
+      for (int i = 0; i < EPL; ++i) A[i] += pp[lane * EPL + i];
     }
-    float out[EPL];
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) out[i] = a.scale * fmaf(-Ds, Cc[i], A[i]);
-    store_row<T, EPL>(a.dq + row * (int64_t)(D * sizeof(T)), lane, out);
-    if (lane % LPH == 0)
-      reinterpret_cast<float2*>(a.stats + row * kSBF<H>)[head] = make_float2(a.lse_in[row * H + head] * kLog2e, Ds);
+    for (int i = 0; i < EPL; ++i) A[i] *= a.scale;
+    store_row<T, EPL>(a.dq + row * (int64_t)(D * sizeof(T)), lane, A);
   }
 }
 
@@ -404,15 +397,16 @@ gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void
   return GT_OK;
 }
 
-gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
-                          const float* lse, const void* dy, void* dq, cudaStream_t st, bool use_logits) {
+gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* y,
+                          const void* halo_kv, const float* lse, const void* dy, void* dq, cudaStream_t st,
+                          bool use_logits) {
+  EntryState e = entry_state(P, 1, use_logits);
+  e.own_c = y;
   GT_TRY(pipe_pass(P, 1, P->w_rows, P->heavy_rows, P->d_part_rowb.as<float>(), q, dy, lse, k, v, halo_kv, nullptr,
-                   dq, nullptr, P->d_stats.as<float>(), st, 0, entry_state(P, 1, use_logits)));
+                   dq, nullptr, P->d_stats.as<float>(), st, 0, e));
   if (P->heavy_rows.nchunks() > 0) {
     MergeArgs m = merge_args(P->heavy_rows, P->d_part_rowb, P->scale);
     m.dq = (char*)dq;
-    m.stats = P->d_stats.as<float>();
-    m.lse_in = lse;
     GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 1, m, st));
   }
   return GT_OK;

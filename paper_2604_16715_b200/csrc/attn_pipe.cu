@@ -119,13 +119,18 @@ struct PC {
   static constexpr int RB = D * (int)sizeof(T);          // bytes of one feature row
   static constexpr int EPL = D / 32;                      // elements per lane
   static constexpr int LB = EPL * (int)sizeof(T);         // bytes per lane of one row (8..64)
+  static constexpr int W = LB / 4;                        // 32-bit words per lane slice
   static constexpr int LPH = 32 / H;                      // lanes per head
   static constexpr int SB = (8 * H + 15) / 16 * 16;       // (LSE2, D) row of the stats array, padded
-  static constexpr int EB = 2 * RB + (PASS == 2 ? SB : 0);                          // bytes per neighbour
-  // own slot: fwd q | rowb q dY lse | colb [k v]   (ES: the column pass reads the (P, dP) the row
-  // pass stored and needs no own-column data)
-  static constexpr int OWN_DY = PASS == 1 ? RB : 0;
-  static constexpr int OWN_LSE = OWN_DY + RB;
+  static constexpr int PDB = sizeof(T) == 2 ? 4 : 8;      // stored (P, dS) of one entry and head: bf16x2 | f32x2
+  // the recompute column pass gathers each in-neighbour's (LSE2, D) block; with stored (P, dS) it does not
+  static constexpr bool STATS = PASS == 2 && !(ES & 1);
+  static constexpr int EB = 2 * RB + (STATS ? SB : 0);                               // bytes per neighbour
+  // own slot: fwd q | rowb [q] dY Y lse | colb [k v]   (the row pass recomputing q.k needs q; with
+  // stored (P, dS) the column pass needs no own-column data)
+  static constexpr int OWN_DY = PASS == 1 ? ((ES & 2) ? 0 : RB) : 0;
+  static constexpr int OWN_Y = OWN_DY + RB;
+  static constexpr int OWN_LSE = OWN_Y + RB;
   static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * H : ((ES & 1) ? 0 : 2 * RB));
 #ifdef GT_PIPE_U  // tuning override (A/B builds)
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : (GT_PIPE_U * H <= 32 ? GT_PIPE_U : 32 / H));
@@ -133,12 +138,12 @@ struct PC {
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
 #endif
   // per-stage entry state gathered into the stage (ES): rowb s2[U][H] f32 (the forward's logits),
-  // colb (P, dP)[U][H] f32x2 (the row pass's)
-  static constexpr int AUX = PASS == 1 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 2 && (ES & 1)) ? U * H * 8 : 0);
+  // colb (P, dS)[U][H] (the row pass's)
+  static constexpr int AUX = PASS == 1 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 2 && (ES & 1)) ? U * H * PDB : 0);
   static constexpr int STAGE = (U * EB + AUX + 15) / 16 * 16;
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
-  // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dP)[U][H]
-  static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * 8 : 0);
+  // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dS)[U][H]
+  static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0);
   static constexpr int WARP_SMEM = kS * (STAGE + OWNP + XS);
   static_assert(LB == 4 || LB == 8 || LB % 16 == 0, "lane slice must be 4, 8 or a multiple of 16 bytes");
   static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
@@ -165,6 +170,7 @@ struct PArgs {
   int64_t n_local;
   const char* oa;        // own tensor A (q | q | k)
   const char* ob;        // own tensor B (- | dy | v)
+  const char* oc;        // own tensor C (- | y | -): the row pass takes D_i = <dY_i, Y_i>
   int64_t own_stride;    // bytes between own rows of the column pass (a feature row, or 2 of them when
                          // the own rows are the [k | v] rows received in the forward)
   const float* lse;      // pass 1: caller's LSE [n_local][H] (natural log)
@@ -174,9 +180,9 @@ struct PArgs {
   float* part;           // chunk partials
   float qscale, scale;
   // materialised entry state (ES kernels; Table 1 keeps U per edge)
-  float* es_out;         // fwd: s2 [nnz_local][H] base-2 logits | rowb: (P, dP) [nnz_local][H][2], both
-                         // in local CSR entry order
-  const float* es_in;    // rowb: s2 | colb: (P, dP)
+  float* es_out;         // fwd: s2 [nnz_local][H] base-2 logits | rowb: (P, dS) [nnz_local][H] (bf16x2 for
+                         // bf16 plans, f32x2 for f32 plans), both in local CSR entry order
+  const float* es_in;    // rowb: s2 | colb: (P, dS)
   const int32_t* src;    // colb: local CSC position -> local CSR entry (read through a window like nbr)
 };
 
@@ -341,6 +347,61 @@ __device__ __forceinline__ float dot_raw(const uint32_t (&a)[W], const uint32_t 
                 make_float2(__uint_as_float(b[i]), __uint_as_float(b[i + 1])), s);
     return s.x + s.y;
   }
+}
+
+// Weight of an accumulation acc += w x, as the 32-bit word that is broadcast between lanes: bf16 plans
+// round it to bf16 (low half; the products w x are then exact in fp32 and summed in fp32, as
+// FlashAttention rounds P and dS before its P V and dS K products), f32 plans keep the fp32 bits.
+template <typename T>
+__device__ __forceinline__ uint32_t wpack(float x) {
+  if constexpr (sizeof(T) == 2) {
+    uint16_t b;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(b) : "f"(x));
+    return (uint32_t)b;
+  } else {
+    return __float_as_uint(x);
+  }
+}
+
+// (P, dS) of one entry and head as stored by the row pass: bf16x2 {lo = P, hi = dS} (bf16 plans)
+__device__ __forceinline__ uint32_t pack_pd_bf16(float p, float ds) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(ds), "f"(p));
+  return r;
+}
+
+// acc += w x over this lane's raw slice x (W storage words).  bf16: w is the bf16 in half HI of wb
+// (FHFMA.BF16 reads both halves of the row words in place: no unpacking); f32: w = the float wb.
+template <typename T, int W, int EPL, bool HI = false>
+__device__ __forceinline__ void accum(uint32_t wb, const uint32_t (&x)[W], float (&acc)[EPL]) {
+  if constexpr (sizeof(T) == 2) {
+    uint16_t wl, wh;
+    asm("mov.b32 {%0, %1}, %2;" : "=h"(wl), "=h"(wh) : "r"(wb));
+    const uint16_t w = HI ? wh : wl;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      uint16_t xl, xh;
+      asm("mov.b32 {%0, %1}, %2;" : "=h"(xl), "=h"(xh) : "r"(x[i]));
+      acc[2 * i] = fma_bf16(w, xl, acc[2 * i]);
+      acc[2 * i + 1] = fma_bf16(w, xh, acc[2 * i + 1]);
+    }
+  } else {
+    const float w = __uint_as_float(wb);
+    const float2 ww = make_float2(w, w);
+#pragma unroll
+    for (int i = 0; i < W; i += 2) {
+      const float2 r = f2fma(ww, make_float2(__uint_as_float(x[i]), __uint_as_float(x[i + 1])),
+                             make_float2(acc[i], acc[i + 1]));
+      acc[i] = r.x;
+      acc[i + 1] = r.y;
+    }
+  }
+}
+
+// predicated 32-bit global store of raw bits
+__device__ __forceinline__ void st_pred_u32(uint32_t* p, uint32_t x, bool on) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;}" ::"l"(p), "r"(x),
+               "r"((int)on) : "memory");
 }
 
 template <int LPH>
@@ -566,7 +627,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       cp_lane_z<LB>(dst + RB, pb, valid);
       // (LSE2, D) block of the neighbour: SB / 16 lanes copy 16 bytes each (read by all lanes of a head
       // after the stage's wait + __syncwarp)
-      if constexpr (PASS == 2) {
+      if constexpr (C::STATS) {
         if (lane < C::SB / 16) cp_async16z(st + u * EB + 2 * RB + lane * 16, ps, valid);
       }
     }
@@ -575,12 +636,15 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       if (lane < U * H)
         cp_async4z(st + U * EB + lane * 4, row_addr(reinterpret_cast<const char*>(a.es_in), (uint32_t)pe * H + (kv ? lane : 0), 4), kv);
     }
-    if constexpr ((ES & 1) && PASS == 2) {  // (P, dP) of the stage's entries, stored in CSR order by the row pass
+    if constexpr ((ES & 1) && PASS == 2) {  // (P, dS) of the stage's entries, stored in CSR order by the row pass
       const int ku = lane / H, kh = lane % H;
       const uint32_t ke = (uint32_t)__shfl_sync(kFull, wsrc, off + ku);
-      if (lane < U * H)
-        cp_async8z(st + U * EB + lane * 8,  // window entries past the item may be remote rows (src -1)
-                   row_addr(reinterpret_cast<const char*>(a.es_in) + kh * 8, ku < cnt ? ke : 0u, H * 8), ku < cnt);
+      // window entries past the item may be remote rows (src -1): masked, and read entry 0 instead
+      const char* src = row_addr(reinterpret_cast<const char*>(a.es_in) + kh * C::PDB, ku < cnt ? ke : 0u, H * C::PDB);
+      if (lane < U * H) {
+        if constexpr (C::PDB == 8) cp_async8z(st + U * EB + lane * 8, src, ku < cnt);
+        else cp_async4z(st + U * EB + lane * 4, src, ku < cnt);
+      }
     }
     md.e0 = pe;
     md.cnt = cnt;
@@ -595,6 +659,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       } else if constexpr (PASS == 1) {
         if constexpr (!(ES & 2)) cp_slice<LB>(o, a.oa + r * RB, lane);
         cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
+        cp_slice<LB>(o + C::OWN_Y, a.oc + r * RB, lane);
         cp_async<4>(o + C::OWN_LSE + head * 4, a.lse + r * H + head);
       } else if constexpr (!(ES & 1)) {
         cp_slice<LB>(o, a.oa + r * a.own_stride, lane);
@@ -607,10 +672,11 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
   };
 
   // ---------------- consumer state ----------------
-  constexpr int W = LB / 4;
-  float q[EPL], g[EPL], acc[EPL], acc2[EPL];
-  uint32_t ow[W];           // raw own-row words: q (fwd) or dY (rowb), dotted with FHFMA / FFMA2
-  float m = 0.f, l = 0.f;   // fwd: running max / sum (base 2); rowb: lse2 (m), D (l)
+  constexpr int W = C::W;
+  float acc[EPL], acc2[EPL];  // fwd: y | rowb: dQ (unscaled) | colb: dK (unscaled), dV (acc2)
+  uint32_t ow[W];             // raw own-row words: q (fwd), dY (rowb), k (colb recompute)
+  uint32_t ow2[W];            // rowb recompute: q; colb recompute: v
+  float m = 0.f, l = 0.f;     // fwd: running max / sum (base 2) | rowb: lse2 (m), D (l)
 
   Meta md[kS];
 #pragma unroll
@@ -622,7 +688,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
       cp_wait<kS - 1>();
-      if constexpr (PASS == 2) __syncwarp();  // stats blocks were copied by other lanes
+      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2))) __syncwarp();  // blocks copied by other lanes
       const Meta cur = md[s];
       if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one
       const char* st = stages + s * C::STAGE;
@@ -635,22 +701,19 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           m = -INFINITY;
           l = 0.f;
         } else if constexpr (PASS == 1) {
-          if constexpr (!(ES & 2)) {
-            lds_f32<T, EPL>(o + lane * LB, q);
-#pragma unroll
-            for (int i = 0; i < EPL; ++i) q[i] *= a.qscale;
-          }
+          if constexpr (!(ES & 2)) lds_raw<W>(o + lane * LB, ow2);
           lds_raw<W>(o + C::OWN_DY + lane * LB, ow);
+          uint32_t yw[W];
+          lds_raw<W>(o + C::OWN_Y + lane * LB, yw);
+          // D_i = sum_e P_e dP_e = <dY_i, sum_e P_e v_j> = <dY_i, Y_i> (Sum_e P_e = 1)
+          l = head_sum<LPH>(dot_raw<T, W>(ow, yw));
           m = reinterpret_cast<const float*>(o + C::OWN_LSE)[head] * kLog2e;
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) { acc[i] = 0.f; acc2[i] = 0.f; }
-          l = 0.f;
+          for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
         } else {
           if constexpr (!(ES & 1)) {
-            lds_f32<T, EPL>(o + lane * LB, q);      // k_j
-            lds_f32<T, EPL>(o + RB + lane * LB, g); // v_j
-#pragma unroll
-            for (int i = 0; i < EPL; ++i) q[i] *= a.qscale;
+            lds_raw<W>(o + lane * LB, ow);       // k_j
+            lds_raw<W>(o + RB + lane * LB, ow2); // v_j
           }
 #pragma unroll
           for (int i = 0; i < EPL; ++i) { acc[i] = 0.f; acc2[i] = 0.f; }
@@ -687,12 +750,13 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         scale2<EPL>(corr, acc);
         const float pl = ex2(sl - mx);  // 0 for masked neighbours
         l += pl;
+        const uint32_t wl = wpack<T>(pl);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float p = __shfl_sync(kFull, pl, B::src(lane, u));
-          float vf[EPL];
-          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
-          axpy<EPL>(p, vf, acc);
+          const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
+          uint32_t vw[W];
+          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+          accum<T, W, EPL>(w, vw, acc);
         }
         m = mx;
       } else if constexpr (PASS == 0) {
@@ -720,107 +784,120 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         for (int u = 0; u < U; ++u) {
           const float p = ex2(sc[u] - mx);  // 0 for masked neighbours
           l += p;
-          float vf[EPL];
-          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, vf);
-          axpy<EPL>(p, vf, acc);
+          uint32_t vw[W];
+          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+          accum<T, W, EPL>(wpack<T>(p), vw, acc);
         }
         m = mx;
-      } else if constexpr (PASS == 1 && kBflyR) {
-        // Row pass with stored logits: the 4 partial dP = <dY_i, v_j> are reduced by the same transposed
-        // butterfly (each lane group ends with one neighbour's dP); p is computed once per lane for
-        // its neighbour, (p, dP) stored, and (p, p dP) broadcast back for the two SpMM accumulators.
-        float part[4];
+      } else if constexpr (PASS == 1) {
+        // Row pass: p_e = 2^(s2_e - lse2_i), dP_e = <dY_i, v_j>, dS_e = p_e (dP_e - D_i) (unscaled),
+        // dQ_i += dS_e k_j; (p, dS) stored per entry for the column pass.
+        if constexpr (kBflyR) {
+          // the 4 partial dP are reduced by the transposed butterfly (each lane group ends with one
+          // neighbour's dP); p and dS are computed once per lane for that neighbour
+          float part[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint32_t vw[W];
-          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
-          part[u] = dot_raw<T, W>(ow, vw);
-        }
-        using B = Bfly<LPH>;
-        const float dpl = B::reduce(part, lane);
-        const int ug = B::group(lane);
-        const float s_ = reinterpret_cast<const float*>(st + U * EB)[ug * H + head];  // forward's logit
-        const float pl = ug < cnt ? ex2(s_ - m) : 0.f;
-        const float pdl = pl * dpl;
-        l += pdl;  // per lane group; summed over the groups at the end of the row
-        if constexpr (ES & 1)  // lanes b0 = 0, 1 write the same 8 bytes
-          reinterpret_cast<float2*>(xs + s * C::XS)[ug * H + head] = make_float2(pl, dpl);
+          for (int u = 0; u < 4; ++u) {
+            uint32_t vw[W];
+            lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+            part[u] = dot_raw<T, W>(ow, vw);
+          }
+          using B = Bfly<LPH>;
+          const float dpl = B::reduce(part, lane);
+          const int ug = B::group(lane);
+          const float s_ = reinterpret_cast<const float*>(st + U * EB)[ug * H + head];  // forward's logit
+          const float pl = ug < cnt ? ex2(s_ - m) : 0.f;
+          const float dsl = pl * (dpl - l);
+          if constexpr (ES & 1) {  // lanes b0 = 0, 1 write the same bytes
+            if constexpr (C::PDB == 4) reinterpret_cast<uint32_t*>(xs + s * C::XS)[ug * H + head] = pack_pd_bf16(pl, dsl);
+            else reinterpret_cast<float2*>(xs + s * C::XS)[ug * H + head] = make_float2(pl, dsl);
+          }
+          const uint32_t wl = wpack<T>(dsl);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int src = B::src(lane, u);
-          const float p = __shfl_sync(kFull, pl, src);
-          const float pd = __shfl_sync(kFull, pdl, src);
-          float kf[EPL];
-          lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
-          axpy<EPL>(pd, kf, acc);
-          axpy<EPL>(p, kf, acc2);
-        }
-        if constexpr (ES & 1) {
-          __syncwarp();
-          const float2* x = reinterpret_cast<const float2*>(xs + s * C::XS);
-          // (same per-stage store as the generic row pass below)
-          const float* xf = reinterpret_cast<const float*>(x);
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
+            uint32_t kw[W];
+            lds_raw<W>(st + u * EB + lane * LB, kw);
+            accum<T, W, EPL>(w, kw, acc);
+          }
+        } else {
+          float pv[U], dsv[U];
 #pragma unroll
-          for (int t = 0; t < (2 * U * H + 31) / 32; ++t) {
-            const int f = lane + 32 * t;
-            st_pred(a.es_out + (int64_t)cur.e0 * (2 * H) + f, xf[f < 2 * U * H ? f : 0], f < 2 * cnt * H);
+          for (int u = 0; u < U; ++u) {
+            uint32_t kw[W], vw[W];
+            lds_raw<W>(st + u * EB + lane * LB, kw);
+            lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+            float s_;
+            if constexpr (ES & 2) s_ = reinterpret_cast<const float*>(st + U * EB)[u * H + head];  // forward's logit
+            else s_ = head_sum<LPH>(dot_raw<T, W>(ow2, kw)) * a.qscale;
+            const float dp = head_sum<LPH>(dot_raw<T, W>(ow, vw));
+            pv[u] = u < cnt ? ex2(s_ - m) : 0.f;
+            dsv[u] = pv[u] * (dp - l);
+            if constexpr (ES & 1) {  // all lanes of a head write the same bytes
+              if constexpr (C::PDB == 4)
+                reinterpret_cast<uint32_t*>(xs + s * C::XS)[u * H + head] = pack_pd_bf16(pv[u], dsv[u]);
+              else reinterpret_cast<float2*>(xs + s * C::XS)[u * H + head] = make_float2(pv[u], dsv[u]);
+            }
+            accum<T, W, EPL>(wpack<T>(dsv[u]), kw, acc);
           }
         }
-      } else if constexpr (PASS == 1) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          float kf[EPL];
-          uint32_t vw[W];
-          lds_f32<T, EPL>(st + u * EB + lane * LB, kf);
-          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
-          float s_;
-          if constexpr (ES & 2) s_ = reinterpret_cast<const float*>(st + U * EB)[u * H + head];  // forward's logit
-          else s_ = head_sum<LPH>(dot<EPL>(q, kf));
-          const float dp = head_sum<LPH>(dot_raw<T, W>(ow, vw));
-          const float p = u < cnt ? ex2(s_ - m) : 0.f;
-          if constexpr (ES & 1)  // all lanes of a head write the same 8 bytes
-            reinterpret_cast<float2*>(xs + s * C::XS)[u * H + head] = make_float2(p, dp);
-          const float pd = p * dp;
-          l += pd;
-          axpy<EPL>(pd, kf, acc);
-          axpy<EPL>(p, kf, acc2);
-        }
         if constexpr (ES & 1) {
-          // (P, dP)[entry e0 + u][head][2] of the stage, transposed through shared memory and written
-          // with one coalesced store per 32 values (the stage's scratch is rewritten two stages later,
-          // after another __syncwarp).
+          // (P, dS)[entry e0 + u][head] of the stage, transposed through shared memory and written with
+          // one coalesced store per 32 words (the stage's scratch is rewritten two stages later, after
+          // another __syncwarp).
+          constexpr int NW = U * H * C::PDB / 4;   // words of the stage
+          constexpr int EW = H * C::PDB / 4;       // words per entry
           __syncwarp();
-          const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
+          const uint32_t* x = reinterpret_cast<const uint32_t*>(xs + s * C::XS);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(a.es_out) + (int64_t)cur.e0 * EW;
 #pragma unroll
-          for (int t = 0; t < (2 * U * H + 31) / 32; ++t) {
+          for (int t = 0; t < (NW + 31) / 32; ++t) {
             const int f = lane + 32 * t;
-            st_pred(a.es_out + (int64_t)cur.e0 * (2 * H) + f, x[f < 2 * U * H ? f : 0], f < 2 * cnt * H);
+            st_pred_u32(dst + f, x[f < NW ? f : 0], f < cnt * EW);
           }
         }
       } else {
+        // Column pass: dV_j += p_e dY_i, dK_j += dS_e q_i (unscaled), with (p, dS) stored by the row pass
+        // or recomputed from q_i, dY_i, (LSE2_i, D_i) and the column's own k_j, v_j.
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          float qf[EPL], gf[EPL];
-          lds_f32<T, EPL>(st + u * EB + lane * LB, qf);
-          lds_f32<T, EPL>(st + u * EB + RB + lane * LB, gf);
-          const float2 sd = reinterpret_cast<const float2*>(st + u * EB + 2 * RB)[head];
-          float p, dp;
+          uint32_t qw[W], gw[W];
+          lds_raw<W>(st + u * EB + lane * LB, qw);
+          lds_raw<W>(st + u * EB + RB + lane * LB, gw);
           if constexpr (ES & 1) {  // stored by the row pass; zero-filled for masked neighbours
-            const float2 e = reinterpret_cast<const float2*>(st + U * EB)[u * H + head];
-            p = e.x;
-            dp = e.y;
+            if constexpr (C::PDB == 4) {
+              const uint32_t e = reinterpret_cast<const uint32_t*>(st + U * EB)[u * H + head];
+              accum<T, W, EPL, false>(e, gw, acc2);  // P (low half)
+              accum<T, W, EPL, true>(e, qw, acc);    // dS (high half)
+            } else {
+              const float2 e = reinterpret_cast<const float2*>(st + U * EB)[u * H + head];
+              accum<T, W, EPL>(__float_as_uint(e.x), gw, acc2);
+              accum<T, W, EPL>(__float_as_uint(e.y), qw, acc);
+            }
           } else {
-            const float s_ = head_sum<LPH>(dot<EPL>(qf, q));
-            dp = head_sum<LPH>(dot<EPL>(gf, g));
-            p = u < cnt ? ex2(s_ - sd.x) : 0.f;
+            const float2 sd = reinterpret_cast<const float2*>(st + u * EB + 2 * RB)[head];
+            const float s_ = head_sum<LPH>(dot_raw<T, W>(qw, ow)) * a.qscale;
+            const float dp = head_sum<LPH>(dot_raw<T, W>(gw, ow2));
+            const float p = u < cnt ? ex2(s_ - sd.x) : 0.f;
+            const float ds = p * (dp - sd.y);
+            if constexpr (sizeof(T) == 2) {
+              const uint32_t e = pack_pd_bf16(p, ds);
+              accum<T, W, EPL, false>(e, gw, acc2);
+              accum<T, W, EPL, true>(e, qw, acc);
+            } else {
+              accum<T, W, EPL>(__float_as_uint(p), gw, acc2);
+              accum<T, W, EPL>(__float_as_uint(ds), qw, acc);
+            }
           }
-          const float ds = p * (dp - sd.y);
-          axpy<EPL>(p, gf, acc2);   // dV
-          axpy<EPL>(ds, qf, acc);   // dK (unscaled)
         }
       }
       if (cur.last) {
         const int32_t own = cur.own;
+        const int64_t r = own >= 0 ? own : 0;
+        if constexpr (PASS == 1) {  // (LSE2, D) of the row (every chunk of a heavy row writes the same values)
+          const int64_t rr = own >= 0 ? own : a.cown[-1 - (int64_t)own];
+          reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + rr * C::SB)[head] = make_float2(m, l);
+        }
         if (own < 0) {  // chunk of a heavy row/column: partial state for the merge kernel
           const int64_t ch = -1 - (int64_t)own;
           if constexpr (PASS == 0 && kBfly) l = Bfly<LPH>::all_sum(l);  // per lane group -> the row's (chunk's) l
@@ -830,18 +907,15 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
             for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
             { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
           } else if constexpr (PASS == 1) {
-            if constexpr (kBflyR) l = Bfly<LPH>::all_sum(l);
-            float* pp = a.part + ch * (int64_t)(2 * D + H);
+            float* pp = a.part + ch * (int64_t)D;
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
-            pp[2 * D + head] = l;
+            for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
           } else {
             float* pp = a.part + ch * (int64_t)(2 * D);
 #pragma unroll
             for (int i = 0; i < EPL; ++i) { pp[lane * EPL + i] = acc[i]; pp[D + lane * EPL + i] = acc2[i]; }
           }
         } else {
-          const int64_t r = own;
           if constexpr (PASS == 0 && kBfly) l = Bfly<LPH>::all_sum(l);
           if constexpr (PASS == 0) {
             const float inv = 1.f / l;
@@ -850,11 +924,9 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
             a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
           } else if constexpr (PASS == 1) {
-            if constexpr (kBflyR) l = Bfly<LPH>::all_sum(l);
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) acc[i] = a.scale * fmaf(-l, acc2[i], acc[i]);
+            for (int i = 0; i < EPL; ++i) acc[i] *= a.scale;
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
-            reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + r * C::SB)[head] = make_float2(m, l);
           } else {
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] *= a.scale;
@@ -1015,6 +1087,7 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.n_local = P->n_local;
   a.oa = (const char*)own_a;
   a.ob = (const char*)own_b;
+  a.oc = (const char*)es.own_c;
   a.lse = lse;
   a.out_a = (char*)out_a;
   a.out_b = (char*)out_b;

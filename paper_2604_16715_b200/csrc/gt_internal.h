@@ -138,7 +138,7 @@ struct gt_plan_s {
   gt::DevBuf d_stats;
   // heavy-chunk workspaces (fp32)
   gt::DevBuf d_part_fwd;           // [forward chunks, D + 2 heads]
-  gt::DevBuf d_part_rowb;          // [row chunks, 2 D + heads]
+  gt::DevBuf d_part_rowb;          // [row chunks, D]
   gt::DevBuf d_part_colb;          // [col chunks, 2 D]
 
   // materialised entry state (opts.edge_state; Table 1 stores U per edge): the row
@@ -147,7 +147,7 @@ struct gt_plan_s {
   bool es = false;
   bool es_logits = false;          // the forward's logits are part of the state (GT_ES_LOGITS, default 1)
   gt::DevBuf d_s2;                 // f32 [nnz_local][heads] base-2 logits of the forward, local CSR order
-  gt::DevBuf d_pd;                 // f32 [nnz_local][heads][2], local CSR order
+  gt::DevBuf d_pd;                 // (P, dS) [nnz_local][heads]: bf16x2 (bf16 plans) | f32x2, local CSR order
   gt::DevBuf d_src;                // int32 [nnz_in_local]: local CSR entry of the CSC position, -1 if remote row
   // column pass with world > 1 and es: phase A = local-row entries (stored state, runs while the
   // in-halo stats are exchanged), phase B = remote-row entries (recompute); split columns merged
@@ -233,7 +233,7 @@ struct gt_plan_s {
 
   // CUDA-graph replay (gt_opts.cuda_graphs, world 1): executable graphs keyed by the tensor pointers
   bool graphs = false, fwd_warm = false, bwd_warm = false;
-  typedef std::array<const void*, 10> GraphKey;
+  typedef std::array<const void*, 11> GraphKey;
   struct GraphEntry {
     GraphKey key;
     cudaGraphExec_t exec;
@@ -266,8 +266,9 @@ gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void
                           cudaStream_t st);
 // use_logits: read the forward's stored logits (false: recompute q.k; the stored ones belong to
 // another forward)
-gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* halo_kv,
-                          const float* lse, const void* dy, void* dq, cudaStream_t st, bool use_logits = true);
+gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* y,
+                          const void* halo_kv, const float* lse, const void* dy, void* dq, cudaStream_t st,
+                          bool use_logits = true);
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,
                           const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st,
                           cudaEvent_t side_ready);
@@ -289,6 +290,7 @@ struct EntryState {
   const int32_t* nbr = nullptr;  // neighbour (row) ids of the entries; null: the plan's CSC slice
   int64_t nnbr = 0;
   int64_t own_stride = 0;        // bytes between own rows (0: one feature row)
+  const void* own_c = nullptr;   // rowb: Y (D_i = <dY_i, Y_i>)
 };
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
                     const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,

@@ -100,7 +100,7 @@ def lib():
         L.gt_plan_info_get.argtypes = [_P, ctypes.POINTER(_Info)]
         L.gt_plan_export.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _I64, ctypes.POINTER(_I64)]
         L.gt_attn_fwd.argtypes = [_P, _P, _P, _P, _P, _P, _P]
-        L.gt_attn_bwd.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.gt_attn_bwd.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.gt_attn_fwd_bwd_host.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
         L.gt_plan_timings.argtypes = [_P, _P, _P]
         L.gt_free.argtypes = [_P]
@@ -392,9 +392,10 @@ class Plan:
                                  lse.data_ptr(), self._stream(stream)))
         return y, lse
 
-    def bwd(self, q, k, v, lse, dy, dq=None, dk=None, dv=None, stream=None):
+    def bwd(self, q, k, v, y, lse, dy, dq=None, dk=None, dv=None, stream=None):
+        """Gradients of sum <dy, Y> w.r.t. q, k, v; y and lse are the forward's outputs for q, k, v."""
         import torch
-        for t, nm in ((q, "q"), (k, "k"), (v, "v"), (dy, "dy")):
+        for t, nm in ((q, "q"), (k, "k"), (v, "v"), (y, "y"), (dy, "dy")):
             self._check_tensor(t, nm)
         self._check_tensor(lse, "lse", lse=True)
         dq = torch.empty_like(q) if dq is None else dq
@@ -402,7 +403,7 @@ class Plan:
         dv = torch.empty_like(v) if dv is None else dv
         for t, nm in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
             self._check_tensor(t, nm)
-        _check(lib().gt_attn_bwd(self.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), lse.data_ptr(),
+        _check(lib().gt_attn_bwd(self.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), y.data_ptr(), lse.data_ptr(),
                                  dy.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), self._stream(stream)))
         return dq, dk, dv
 
@@ -445,13 +446,13 @@ def _autograd():
             q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
             y, lse = plan.fwd(q, k, v)
             ctx.plan = plan
-            ctx.save_for_backward(q, k, v, lse)
+            ctx.save_for_backward(q, k, v, y, lse)
             return y
 
         @staticmethod
         def backward(ctx, dy):
-            q, k, v, lse = ctx.saved_tensors
-            dq, dk, dv = ctx.plan.bwd(q, k, v, lse, dy.contiguous())
+            q, k, v, y, lse = ctx.saved_tensors
+            dq, dk, dv = ctx.plan.bwd(q, k, v, y, lse, dy.contiguous())
             return None, dq, dk, dv
 
     return SparseGraphAttention

@@ -36,7 +36,7 @@ def test_fullsize_sampled(cfg_name):
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale)   # bench.py's launch configuration
     dev = {nm: torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).cuda() for nm, x in feats.items()}
     y, lse = plan.fwd(dev["q"], dev["k"], dev["v"])
-    dq, dk, dv = plan.bwd(dev["q"], dev["k"], dev["v"], lse, dev["dy"])
+    dq, dk, dv = plan.bwd(dev["q"], dev["k"], dev["v"], y, lse, dev["dy"])
     torch.cuda.synchronize()
     rng = np.random.default_rng(5)
     rows = sample_ids(np.diff(rp), rng)

@@ -43,7 +43,7 @@ def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=
             s.synchronize()
             for _ in range(steps):  # repeated steps exercise the reuse of exchange / publish buffers
                 y, lse = plan.fwd(tq, tk, tv, stream=s)
-                dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy, stream=s)
+                dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy, stream=s)
             s.synchronize()
             ex = {w: plan.export(w) for w in ("bounds", "halo_out", "halo_in")}
             ex["send_out"] = [plan.export("send_out", p) for p in range(world)]

@@ -34,7 +34,7 @@ def run_case(gt, row_ptr, col_idx, h, d, dtype, seed, scale=None, qk_scale=1.0, 
     assert plan.info()["edge_state"] == (0 if edge_state < 0 else 1)
     tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
     y, lse = plan.fwd(tq, tk, tv)
-    dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy)
+    dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
     torch.cuda.synchronize()
     Y, LSE = oracle.forward(row_ptr, col_idx, q, k, v, scale)
     DQ, DK, DV, _ = oracle.backward(row_ptr, col_idx, q, k, v, dy, scale)
@@ -123,7 +123,7 @@ def test_csc_bitexact_and_deterministic(gt, edge_state):
     # bitwise run-to-run determinism (no atomics in the numerics)
     tq, tk, tv, tdy = ins
     y2, lse2 = plan.fwd(tq, tk, tv)
-    dq2, dk2, dv2 = plan.bwd(tq, tk, tv, lse2, tdy)
+    dq2, dk2, dv2 = plan.bwd(tq, tk, tv, y2, lse2, tdy)
     torch.cuda.synchronize()
     for a, b in zip(outs, (y2, lse2, dq2, dk2, dv2)):
         assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
@@ -192,17 +192,17 @@ def test_errors_are_reported(gt):
         lambda: plan.fwd(z, z, torch.zeros((4, 64, 4), device="cuda").transpose(1, 2)),  # layout
         lambda: plan.fwd(z, z, z, y=torch.zeros((2, 4, 64), device="cuda")),            # output shape
         lambda: plan.fwd(z, z, z, lse=torch.zeros((4, 4), dtype=torch.float64, device="cuda")),
-        lambda: plan.bwd(z, z, z, torch.zeros((4, 3), device="cuda"), z),              # lse shape
-        lambda: plan.bwd(z, z, z, lz.to(torch.bfloat16), z),                           # lse dtype
-        lambda: plan.bwd(z, z, z, lz, z, dq=torch.zeros((5, 4, 64), device="cuda")),   # output shape
-        lambda: plan.bwd(z.cpu(), z, z, lz, z),                                        # device
+        lambda: plan.bwd(z, z, z, z, torch.zeros((4, 3), device="cuda"), z),              # lse shape
+        lambda: plan.bwd(z, z, z, z, lz.to(torch.bfloat16), z),                           # lse dtype
+        lambda: plan.bwd(z, z, z, z, lz, z, dq=torch.zeros((5, 4, 64), device="cuda")),   # output shape
+        lambda: plan.bwd(z.cpu(), z, z, z, lz, z),                                        # device
     ]
     for i, f in enumerate(bad_cases):
         with pytest.raises(gt.GTError) as e:
             f()
         assert e.value.status == 1, i  # GT_EINVAL
     # a backward with no forward before it is no longer an error: it recomputes (test_gpu_state_binding)
-    plan.bwd(z, z, z, lz, z)
+    plan.bwd(z, z, z, z, lz, z)
     torch.cuda.synchronize()
     plan.close()
 
@@ -218,7 +218,7 @@ def test_cuda_graph_replay_matches_eager(gt):
     tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
     eager = gt.Plan(rp, ci, h, d, dtype="bf16", scale=scale, heavy_threshold=64)
     y0, l0 = eager.fwd(tq, tk, tv)
-    g0 = eager.bwd(tq, tk, tv, l0, tdy)
+    g0 = eager.bwd(tq, tk, tv, y0, l0, tdy)
     s = torch.cuda.Stream()
     plan = gt.Plan(rp, ci, h, d, dtype="bf16", scale=scale, heavy_threshold=64, cuda_graphs=True)
     outs = []
@@ -229,7 +229,7 @@ def test_cuda_graph_replay_matches_eager(gt):
         y, lse = bufs[it % 2]
         dq, dk, dv = gbufs[it % 2]
         plan.fwd(tq, tk, tv, y, lse, stream=s)
-        plan.bwd(tq, tk, tv, lse, tdy, dq, dk, dv, stream=s)
+        plan.bwd(tq, tk, tv, y, lse, tdy, dq, dk, dv, stream=s)
         s.synchronize()
         outs.append(tuple(t.clone() for t in (y, lse, dq, dk, dv)))
     torch.cuda.synchronize()
@@ -240,3 +240,28 @@ def test_cuda_graph_replay_matches_eager(gt):
                                b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
     Y, _ = oracle.forward(rp, ci, q, k, v, scale)
     assert normwise(to_f64(outs[-1][0]), Y) <= 2e-2
+
+
+def test_host_buffer_entry_point_with_graph_replay(gt):
+    """gt_attn_fwd_bwd_host on a cuda_graphs plan and a non-default stream: from the third call on the
+    backward is replayed from a graph, and the dQ copy must still wait for the replayed row pass
+    (ev_dq is an external event node of the graph)."""
+    import torch
+    rp, ci = gtgen.random_graph(1500, 22000, seed=62, power=2.2)
+    h, d = 4, 64
+    n = len(rp) - 1
+    q, k, v, dy = inputs(n, h, d, "bf16", 602)
+    plan = gt.Plan(rp, ci, h, d, dtype="bf16", cuda_graphs=True, heavy_threshold=64)
+    pin = lambda x: to_torch(x, "cpu").pin_memory()  # noqa: E731
+    tq, tk, tv, tdy = (pin(x) for x in (q, k, v, dy))
+    Y, LSE = oracle.forward(rp, ci, q, k, v, plan.scale)
+    DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, plan.scale)
+    s = torch.cuda.Stream()
+    for it in range(4):
+        y, dq, dk, dv = (torch.full_like(tq, float("nan")).pin_memory() for _ in range(4))
+        lse = torch.empty((n, h), dtype=torch.float32).pin_memory()
+        plan.fwd_bwd_host(tq, tk, tv, tdy, y, lse, dq, dk, dv, stream=s)
+        assert normwise(to_f64(y), Y) <= 2e-2 and normwise(to_f64(dq), DQ) <= 2e-2, it
+        assert normwise(to_f64(dk), DK) <= 2e-2 and normwise(to_f64(dv), DV) <= 2e-2, it
+        check_lse(lse.numpy(), LSE, "bf16")
+    plan.close()

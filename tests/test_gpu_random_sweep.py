@@ -36,7 +36,7 @@ def test_random_sweep(case):
     plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, heavy_threshold=heavy, edge_state=es)
     tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
     y, lse = plan.fwd(tq, tk, tv)
-    dq, dk, dv = plan.bwd(tq, tk, tv, lse, tdy)
+    dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
     torch.cuda.synchronize()
     Y, LSE = oracle.forward(rp, ci, q, k, v, scale)
     DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, scale)

@@ -59,9 +59,9 @@ def test_interleaved_forwards_world1(dtype, h, d, cuda_graphs):
         for rep in range(3 if cuda_graphs else 1):  # graph mode: eager, capture, replay
             ya, la = plan.fwd(*ta[:3], stream=s)
             yb, lb = plan.fwd(*tb[:3], stream=s)
-            ga = plan.bwd(*ta[:3], la, ta[3], stream=s)   # stale: B's logits are in the plan
-            gb = plan.bwd(*tb[:3], lb, tb[3], stream=s)   # fresh
-            gb2 = plan.bwd(*tb[:3], lb, tb[3], stream=s)  # fresh again (state not consumed)
+            ga = plan.bwd(*ta[:3], ya, la, ta[3], stream=s)   # stale: B's logits are in the plan
+            gb = plan.bwd(*tb[:3], yb, lb, tb[3], stream=s)   # fresh
+            gb2 = plan.bwd(*tb[:3], yb, lb, tb[3], stream=s)  # fresh again (state not consumed)
             outs[rep] = (ya, la, ga, yb, lb, gb, gb2)
     s.synchronize()
     info = plan.info()
@@ -142,8 +142,8 @@ def _loopback_interleaved(rp, ci, h, d, dtype, world, strategy, transport=0, bwd
                 b = [t[lo:hi].contiguous() for t in fb]
                 ya, la = plan.fwd(*a[:3], stream=s)
                 yb, lb = plan.fwd(*b[:3], stream=s)
-                ga = plan.bwd(*a[:3], la, a[3], stream=s)  # stale on every rank
-                gb = plan.bwd(*b[:3], lb, b[3], stream=s)  # fresh
+                ga = plan.bwd(*a[:3], ya, la, a[3], stream=s)  # stale on every rank
+                gb = plan.bwd(*b[:3], yb, lb, b[3], stream=s)  # fresh
             s.synchronize()
             res[r] = ([to_f64(t) for t in (ya, la, *ga)], [to_f64(t) for t in (yb, lb, *gb)], plan.info())
             plan.close()

@@ -26,7 +26,7 @@ for cname in sys.argv[1:] or ["C1", "C2"]:
 
         def step():
             plan.fwd(q, k, v, y, lse, stream=s)
-            plan.bwd(q, k, v, lse, dy, dq, dk, dv, stream=s)
+            plan.bwd(q, k, v, y, lse, dy, dq, dk, dv, stream=s)
         for _ in range(5):
             step()
         s.synchronize()

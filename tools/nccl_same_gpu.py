@@ -31,7 +31,7 @@ lo, hi = plan.row_lo, plan.row_hi
 t = [to_torch(x)[lo:hi].contiguous() for x in (q, k, v, dy)]
 for _ in range(2):
     y, lse = plan.fwd(t[0], t[1], t[2])
-    dq, dk, dv = plan.bwd(t[0], t[1], t[2], lse, t[3])
+    dq, dk, dv = plan.bwd(t[0], t[1], t[2], y, lse, t[3])
 torch.cuda.synchronize()
 Y, _ = oracle.forward(rp, ci, q, k, v, scale)
 DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, scale)

@@ -18,6 +18,6 @@ plan = gt.Plan(rp, ci, h, d, dtype="bf16", heavy_threshold=48, edge_state=es)
 y, lse = plan.fwd(q, k, v)
 torch.cuda.synchronize()
 print("fwd ok", flush=True)
-dq, dk, dv = plan.bwd(q, k, v, lse, dy)
+dq, dk, dv = plan.bwd(q, k, v, y, lse, dy)
 torch.cuda.synchronize()
 print("bwd ok", flush=True)

@@ -31,7 +31,7 @@ def run(world, strategy, h, d, dtype, **kw):
             s.synchronize()
             for _ in range(2):
                 y, lse = plan.fwd(t[0], t[1], t[2], stream=s)
-                plan.bwd(t[0], t[1], t[2], lse, t[3], stream=s)
+                plan.bwd(t[0], t[1], t[2], y, lse, t[3], stream=s)
             s.synchronize()
             plan.close()
         except Exception as e:
