@@ -34,12 +34,15 @@
 // stage.  kS * U neighbours (8 KB at D = 256 bf16) stay in flight per warp, across row boundaries,
 // without occupying registers.  (Measured alternatives - a TMA cp.async.bulk variant, lane-group
 // producers, half-warp rows - are in DESIGN.md section 6.)
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 
@@ -60,6 +63,9 @@ constexpr int kMaxDevices = 64;
 #endif
 #ifndef GT_PIPE_GRAB
 #define GT_PIPE_GRAB 2
+#endif
+#ifndef GT_PIPE_TMA
+#define GT_PIPE_TMA 1
 #endif
 constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
 constexpr int kS = GT_PIPE_STAGES;      // stages per warp (2 measured best: more resident warps)
@@ -97,6 +103,36 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ---- mbarrier + TMA (sm_100a) ----
+__device__ __forceinline__ void mbar_init(void* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(void* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;}"
+                 : "=r"(ok) : "r"(su32(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+// 4 rows (r0..r3) of a 2-D tensor map, columns [c, c + box), into dst (rows contiguous); completion is
+// counted in bytes on `bar`.  Rows outside the tensor are zero-filled.
+__device__ __forceinline__ void tma_gather4(const void* map, void* dst, void* bar, int c, int r0, int r1, int r2,
+                                            int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(dst)), "l"(map), "r"(su32(bar)), "r"(c), "r"(r0),
+      "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct TmaMaps {   // tensor maps of the two gathered tables (k | q, v | dY): [rows][D] elements
+  CUtensorMap a, b;
+};
 
 // predicated global store (no branch, so the warp stays provably converged for the shuffles)
 __device__ __forceinline__ void st_pred(float* p, float x, bool on) {
@@ -140,11 +176,20 @@ struct PC {
   // per-stage entry state gathered into the stage (ES): rowb s2[U][H] f32 (the forward's logits),
   // colb (P, dS)[U][H] (the row pass's)
   static constexpr int AUX = PASS == 1 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 2 && (ES & 1)) ? U * H * PDB : 0);
-  static constexpr int STAGE = (U * EB + AUX + 15) / 16 * 16;
+  // TMA gathers (sm_100 cp.async.bulk.tensor tile::gather4: 4 rows of a 2-D tensor map per instruction)
+  // for the two feature rows of every neighbour when the stage holds exactly 4 neighbours; the
+  // stage then keeps the 4 first rows (k | q) contiguous, then the 4 second rows (v | dY), then stats
+  static constexpr bool TMA = GT_PIPE_TMA && U == 4;
+  static constexpr int STAGE = (U * EB + AUX + 127) / 128 * 128;   // 128-byte aligned TMA destinations
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
   // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dS)[U][H]
   static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0);
-  static constexpr int WARP_SMEM = kS * (STAGE + OWNP + XS);
+  static constexpr int MB = TMA ? kS * 8 : 0;                       // one mbarrier per stage
+  static constexpr int WARP_SMEM = (kS * (STAGE + OWNP + XS) + MB + 127) / 128 * 128;
+  // byte offsets in a stage of neighbour u's first row, second row and (LSE2, D) block
+  static __device__ __forceinline__ int koff(int u) { return TMA ? u * RB : u * EB; }
+  static __device__ __forceinline__ int voff(int u) { return TMA ? U * RB + u * RB : u * EB + RB; }
+  static __device__ __forceinline__ int soff(int u) { return TMA ? 2 * U * RB + u * SB : u * EB + 2 * RB; }
   static_assert(LB == 4 || LB == 8 || LB % 16 == 0, "lane slice must be 4, 8 or a multiple of 16 bytes");
   static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
 };
@@ -465,7 +510,8 @@ template <int PASS, int ES, int EPL>
 constexpr int min_ctas() { return EPL > 8 ? 1 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : 1)); }
 
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
-__global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) pipe_kernel(PArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
+    pipe_kernel(const PArgs a, const __grid_constant__ TmaMaps tm) {
   static_assert(!((ES & 1) && PASS == 2 && HALO), "the ES column pass reads local rows only");
   using C = PC<T, H, D, PASS, ES>;
   constexpr int EPL = C::EPL, LPH = C::LPH, RB = C::RB, EB = C::EB, U = C::U, LB = C::LB;
@@ -484,6 +530,17 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
   char* const stages = smem + (size_t)wid * C::WARP_SMEM;   // kS * STAGE
   char* const owns = stages + kS * C::STAGE;                 // kS * OWNP
   char* const xs = owns + kS * C::OWNP;                      // kS * XS
+  char* const mbar = xs + kS * C::XS;                        // kS mbarriers (TMA)
+  constexpr bool kTma = C::TMA && !HALO;
+  uint32_t phase = 0;                                        // parity of each stage's next mbarrier phase
+  if constexpr (kTma) {
+    if (lane == 0) {
+      for (int s = 0; s < kS; ++s) mbar_init(mbar + 8 * s, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      fence_proxy_async();
+    }
+    __syncwarp();
+  }
 
   // ---------------- producer state (warp-uniform; per-lane only the tables) ----------------
   const int32_t nitems = (int32_t)a.nitems;
@@ -595,6 +652,31 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
     const int off = (int)(pe - win_base);
     const int cnt = min(min((int)(pe_end - pe), 32 - off), U);
     char* st = stages + s * C::STAGE;
+    if constexpr (kTma) {
+      // one lane issues two gather4 copies (the 4 neighbours' first and second rows); masked neighbours
+      // get an out-of-range row (zero-filled by the TMA unit).  The stage was just read with generic
+      // loads by the whole warp: order those before the async-proxy writes.
+      int id[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int cv = __shfl_sync(kFull, win, off + u);
+        id[u] = u < cnt ? cv : (int)n_loc;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(mbar + 8 * s, 2 * U * RB);
+        tma_gather4(&tm.a, st, mbar + 8 * s, 0, id[0], id[1], id[2], id[3]);
+        tma_gather4(&tm.b, st + U * RB, mbar + 8 * s, 0, id[0], id[1], id[2], id[3]);
+      }
+      if constexpr (C::STATS) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (lane < C::SB / 16)
+            cp_async16z(st + C::soff(u) + lane * 16, row_addr(gs_l, (uint32_t)(u < cnt ? id[u] : id[0]), C::SB),
+                        u < cnt);
+      }
+    } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // branch-free: neighbours u >= cnt are zero-filled, not read
       const bool valid = u < cnt;
@@ -630,6 +712,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       if constexpr (C::STATS) {
         if (lane < C::SB / 16) cp_async16z(st + u * EB + 2 * RB + lane * 16, ps, valid);
       }
+    }
     }
     if constexpr ((ES & 2) && PASS == 1) {  // s2 of the stage's entries (contiguous), stored by the forward
       const bool kv = lane < cnt * H;
@@ -690,7 +773,11 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
       cp_wait<kS - 1>();
       if constexpr (PASS == 2 || (PASS == 1 && (ES & 2))) __syncwarp();  // blocks copied by other lanes
       const Meta cur = md[s];
-      if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one
+      if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one (no copy in flight)
+      if constexpr (kTma) {
+        mbar_wait(mbar + 8 * s, (phase >> s) & 1u);
+        phase ^= 1u << s;
+      }
       const char* st = stages + s * C::STAGE;
       if (cur.first) {
         const char* o = owns + s * C::OWNP;
@@ -730,7 +817,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint32_t kw[W];
-          lds_raw<W>(st + u * EB + lane * LB, kw);
+          lds_raw<W>(st + C::koff(u) + lane * LB, kw);
           part[u] = dot_raw<T, W>(ow, kw);
         }
         using B = Bfly<LPH>;
@@ -755,7 +842,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
         for (int u = 0; u < 4; ++u) {
           const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
           uint32_t vw[W];
-          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+          lds_raw<W>(st + C::voff(u) + lane * LB, vw);
           accum<T, W, EPL>(w, vw, acc);
         }
         m = mx;
@@ -764,7 +851,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           uint32_t kw[W];
-          lds_raw<W>(st + u * EB + lane * LB, kw);
+          lds_raw<W>(st + C::koff(u) + lane * LB, kw);
           const float sv = head_sum<LPH>(dot_raw<T, W>(ow, kw)) * a.qscale;
           sc[u] = u < cnt ? sv : -INFINITY;
           if constexpr (ES & 2) reinterpret_cast<float*>(xs + s * C::XS)[u * H + head] = sv;  // head lanes agree
@@ -785,7 +872,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           const float p = ex2(sc[u] - mx);  // 0 for masked neighbours
           l += p;
           uint32_t vw[W];
-          lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+          lds_raw<W>(st + C::voff(u) + lane * LB, vw);
           accum<T, W, EPL>(wpack<T>(p), vw, acc);
         }
         m = mx;
@@ -799,7 +886,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             uint32_t vw[W];
-            lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+            lds_raw<W>(st + C::voff(u) + lane * LB, vw);
             part[u] = dot_raw<T, W>(ow, vw);
           }
           using B = Bfly<LPH>;
@@ -817,7 +904,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
           for (int u = 0; u < 4; ++u) {
             const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
             uint32_t kw[W];
-            lds_raw<W>(st + u * EB + lane * LB, kw);
+            lds_raw<W>(st + C::koff(u) + lane * LB, kw);
             accum<T, W, EPL>(w, kw, acc);
           }
         } else {
@@ -825,8 +912,8 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             uint32_t kw[W], vw[W];
-            lds_raw<W>(st + u * EB + lane * LB, kw);
-            lds_raw<W>(st + u * EB + RB + lane * LB, vw);
+            lds_raw<W>(st + C::koff(u) + lane * LB, kw);
+            lds_raw<W>(st + C::voff(u) + lane * LB, vw);
             float s_;
             if constexpr (ES & 2) s_ = reinterpret_cast<const float*>(st + U * EB)[u * H + head];  // forward's logit
             else s_ = head_sum<LPH>(dot_raw<T, W>(ow2, kw)) * a.qscale;
@@ -862,8 +949,8 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           uint32_t qw[W], gw[W];
-          lds_raw<W>(st + u * EB + lane * LB, qw);
-          lds_raw<W>(st + u * EB + RB + lane * LB, gw);
+          lds_raw<W>(st + C::koff(u) + lane * LB, qw);
+          lds_raw<W>(st + C::voff(u) + lane * LB, gw);
           if constexpr (ES & 1) {  // stored by the row pass; zero-filled for masked neighbours
             if constexpr (C::PDB == 4) {
               const uint32_t e = reinterpret_cast<const uint32_t*>(st + U * EB)[u * H + head];
@@ -875,7 +962,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>())) p
               accum<T, W, EPL>(__float_as_uint(e.y), qw, acc);
             }
           } else {
-            const float2 sd = reinterpret_cast<const float2*>(st + u * EB + 2 * RB)[head];
+            const float2 sd = reinterpret_cast<const float2*>(st + C::soff(u))[head];
             const float s_ = head_sum<LPH>(dot_raw<T, W>(qw, ow)) * a.qscale;
             const float dp = head_sum<LPH>(dot_raw<T, W>(gw, ow2));
             const float p = u < cnt ? ex2(s_ - sd.x) : 0.f;
@@ -975,6 +1062,31 @@ gt_status fill_empty(int pass, const int32_t* ids, int64_t n, char* out_a, char*
 }
 
 // ----------------------------------------------------------------- launcher --
+// Tensor map of a gathered table: `rows` rows of D elements, `stride` bytes apart; box = one row (the
+// gather4 instruction supplies 4 row coordinates).  Encoded on the host per launch (pointers change).
+static gt_status encode_rows(CUtensorMap* m, const void* base, int64_t rows, int D, int elt, int64_t stride) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!enc) return fail(GT_ECUDA, "cuTensorMapEncodeTiled is not available");
+  const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)stride};
+  const cuuint32_t box[2] = {(cuuint32_t)D, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, elt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GT_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return GT_OK;
+}
+
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
 gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
   using C = PC<T, H, D, PASS, ES>;
@@ -1007,8 +1119,14 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
   if (reserve_sms > 0)  // leave SMs free for concurrent communication kernels (overlap phases)
     cap = std::max(1, grid - grid / sms * reserve_sms);
   const int g = (int)std::min<int64_t>(cap, (want + kWarps - 1) / kWarps);
+  TmaMaps tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if constexpr (C::TMA && !HALO) {
+    GT_TRY(encode_rows(&tm.a, a.ga, a.n_local, D, (int)sizeof(T), C::RB));
+    GT_TRY(encode_rows(&tm.b, a.gb, a.n_local, D, (int)sizeof(T), C::RB));
+  }
   GT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
-  pipe_kernel<T, H, D, PASS, HALO, ES><<<g, kWarps * 32, smem, st>>>(a);
+  pipe_kernel<T, H, D, PASS, HALO, ES><<<g, kWarps * 32, smem, st>>>(a, tm);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
 }

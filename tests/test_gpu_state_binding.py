@@ -84,9 +84,11 @@ def test_backward_without_forward_world1():
     A = inputs(n, h, d, "bf16", 3021)
     ref = _ref(rp, ci, A, scale)
     ta = [to_torch(x) for x in A]
-    lse = to_torch(np.ascontiguousarray(ref[1], np.float32))  # the forward ran elsewhere (another plan)
+    # the forward ran elsewhere (here: the oracle's Y and LSE, rounded to the plan's types)
+    lse = to_torch(np.ascontiguousarray(ref[1], np.float32))
+    y = to_torch(gtgen.f32_to_bf16_bits(np.ascontiguousarray(ref[0], np.float32)))
     plan = gt.Plan(rp, ci, h, d, dtype="bf16", scale=scale, edge_state=1)
-    g = plan.bwd(*ta[:3], lse, ta[3])
+    g = plan.bwd(*ta[:3], y, lse, ta[3])
     torch.cuda.synchronize()
     _check((None, None, *(to_f64(t) for t in g)), ref, "bf16", "bwd-only")
     assert plan.info()["stale_bwds"] == 1
