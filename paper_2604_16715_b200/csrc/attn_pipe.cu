@@ -186,10 +186,11 @@ struct PC {
   static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0);
   static constexpr int MB = TMA ? kS * 8 : 0;                       // one mbarrier per stage
   static constexpr int WARP_SMEM = (kS * (STAGE + OWNP + XS) + MB + 127) / 128 * 128;
-  // byte offsets in a stage of neighbour u's first row, second row and (LSE2, D) block
-  static __device__ __forceinline__ int koff(int u) { return TMA ? u * RB : u * EB; }
-  static __device__ __forceinline__ int voff(int u) { return TMA ? U * RB + u * RB : u * EB + RB; }
-  static __device__ __forceinline__ int soff(int u) { return TMA ? 2 * U * RB + u * SB : u * EB + 2 * RB; }
+  // byte offsets in a stage of neighbour u's first row, second row and (LSE2, D) block (tma: the kernel
+  // gathers with TMA; kernels with remote rows keep the interleaved per-lane-copy layout)
+  template <bool TM> static __device__ __forceinline__ int koff(int u) { return TM ? u * RB : u * EB; }
+  template <bool TM> static __device__ __forceinline__ int voff(int u) { return TM ? U * RB + u * RB : u * EB + RB; }
+  template <bool TM> static __device__ __forceinline__ int soff(int u) { return TM ? 2 * U * RB + u * SB : u * EB + 2 * RB; }
   static_assert(LB == 4 || LB == 8 || LB % 16 == 0, "lane slice must be 4, 8 or a multiple of 16 bytes");
   static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
 };
@@ -673,7 +674,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (lane < C::SB / 16)
-            cp_async16z(st + C::soff(u) + lane * 16, row_addr(gs_l, (uint32_t)(u < cnt ? id[u] : id[0]), C::SB),
+            cp_async16z(st + C::template soff<kTma>(u) + lane * 16, row_addr(gs_l, (uint32_t)(u < cnt ? id[u] : id[0]), C::SB),
                         u < cnt);
       }
     } else {
@@ -817,7 +818,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint32_t kw[W];
-          lds_raw<W>(st + C::koff(u) + lane * LB, kw);
+          lds_raw<W>(st + C::template koff<kTma>(u) + lane * LB, kw);
           part[u] = dot_raw<T, W>(ow, kw);
         }
         using B = Bfly<LPH>;
@@ -842,7 +843,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         for (int u = 0; u < 4; ++u) {
           const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
           uint32_t vw[W];
-          lds_raw<W>(st + C::voff(u) + lane * LB, vw);
+          lds_raw<W>(st + C::template voff<kTma>(u) + lane * LB, vw);
           accum<T, W, EPL>(w, vw, acc);
         }
         m = mx;
@@ -851,7 +852,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           uint32_t kw[W];
-          lds_raw<W>(st + C::koff(u) + lane * LB, kw);
+          lds_raw<W>(st + C::template koff<kTma>(u) + lane * LB, kw);
           const float sv = head_sum<LPH>(dot_raw<T, W>(ow, kw)) * a.qscale;
           sc[u] = u < cnt ? sv : -INFINITY;
           if constexpr (ES & 2) reinterpret_cast<float*>(xs + s * C::XS)[u * H + head] = sv;  // head lanes agree
@@ -872,7 +873,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
           const float p = ex2(sc[u] - mx);  // 0 for masked neighbours
           l += p;
           uint32_t vw[W];
-          lds_raw<W>(st + C::voff(u) + lane * LB, vw);
+          lds_raw<W>(st + C::template voff<kTma>(u) + lane * LB, vw);
           accum<T, W, EPL>(wpack<T>(p), vw, acc);
         }
         m = mx;
@@ -886,7 +887,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             uint32_t vw[W];
-            lds_raw<W>(st + C::voff(u) + lane * LB, vw);
+            lds_raw<W>(st + C::template voff<kTma>(u) + lane * LB, vw);
             part[u] = dot_raw<T, W>(ow, vw);
           }
           using B = Bfly<LPH>;
@@ -904,7 +905,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
           for (int u = 0; u < 4; ++u) {
             const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
             uint32_t kw[W];
-            lds_raw<W>(st + C::koff(u) + lane * LB, kw);
+            lds_raw<W>(st + C::template koff<kTma>(u) + lane * LB, kw);
             accum<T, W, EPL>(w, kw, acc);
           }
         } else {
@@ -912,8 +913,8 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             uint32_t kw[W], vw[W];
-            lds_raw<W>(st + C::koff(u) + lane * LB, kw);
-            lds_raw<W>(st + C::voff(u) + lane * LB, vw);
+            lds_raw<W>(st + C::template koff<kTma>(u) + lane * LB, kw);
+            lds_raw<W>(st + C::template voff<kTma>(u) + lane * LB, vw);
             float s_;
             if constexpr (ES & 2) s_ = reinterpret_cast<const float*>(st + U * EB)[u * H + head];  // forward's logit
             else s_ = head_sum<LPH>(dot_raw<T, W>(ow2, kw)) * a.qscale;
@@ -949,8 +950,8 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           uint32_t qw[W], gw[W];
-          lds_raw<W>(st + C::koff(u) + lane * LB, qw);
-          lds_raw<W>(st + C::voff(u) + lane * LB, gw);
+          lds_raw<W>(st + C::template koff<kTma>(u) + lane * LB, qw);
+          lds_raw<W>(st + C::template voff<kTma>(u) + lane * LB, gw);
           if constexpr (ES & 1) {  // stored by the row pass; zero-filled for masked neighbours
             if constexpr (C::PDB == 4) {
               const uint32_t e = reinterpret_cast<const uint32_t*>(st + U * EB)[u * H + head];
@@ -962,7 +963,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
               accum<T, W, EPL>(__float_as_uint(e.y), qw, acc);
             }
           } else {
-            const float2 sd = reinterpret_cast<const float2*>(st + C::soff(u))[head];
+            const float2 sd = reinterpret_cast<const float2*>(st + C::template soff<kTma>(u))[head];
             const float s_ = head_sum<LPH>(dot_raw<T, W>(qw, ow)) * a.qscale;
             const float dp = head_sum<LPH>(dot_raw<T, W>(gw, ow2));
             const float p = u < cnt ? ex2(s_ - sd.x) : 0.f;
