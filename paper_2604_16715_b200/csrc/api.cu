@@ -1042,12 +1042,19 @@ static gt_status fwd_exchange(gt_plan_t P, const void* k, const void* v, cudaStr
 }
 
 static void set_fwd_tag(gt_plan_t P, const void* q, const void* k, const void* v, const void* lse) {
-  P->fwd_tag[0] = q;
-  P->fwd_tag[1] = k;
-  P->fwd_tag[2] = v;
-  P->fwd_tag[3] = lse;
+  P->kv_tag[0] = k;
+  P->kv_tag[1] = v;
+  P->kv_valid = true;
+  P->lg_tag[0] = q;
+  P->lg_tag[1] = k;
+  P->lg_tag[2] = v;
+  P->lg_tag[3] = lse;
+  P->lg_valid = true;
+  P->slice_tag[0] = q;
+  P->slice_tag[1] = k;
+  P->slice_tag[2] = v;
+  P->slice_valid = true;
   P->fwd_gen++;
-  P->fwd_done = true;
 }
 
 // Records `ev` on `st`; under stream capture as an external event node, so that replaying the graph
@@ -1060,9 +1067,15 @@ static gt_status record_external(cudaEvent_t ev, cudaStream_t st) {
   return GT_OK;
 }
 
-// True when the plan's retained forward state belongs to the forward of these tensors.
-static bool fwd_fresh(gt_plan_t P, const void* q, const void* k, const void* v, const void* lse) {
-  return P->fwd_done && P->fwd_tag[0] == q && P->fwd_tag[1] == k && P->fwd_tag[2] == v && P->fwd_tag[3] == lse;
+// Which retained pieces belong to these tensors (gt_plan_s tags).
+static bool logits_fresh(gt_plan_t P, const void* q, const void* k, const void* v, const void* lse) {
+  return P->lg_valid && P->lg_tag[0] == q && P->lg_tag[1] == k && P->lg_tag[2] == v && P->lg_tag[3] == lse;
+}
+static bool kv_fresh(gt_plan_t P, const void* k, const void* v) {
+  return P->kv_valid && P->kv_tag[0] == k && P->kv_tag[1] == v;
+}
+static bool slices_fresh(gt_plan_t P, const void* q, const void* k, const void* v) {
+  return P->slice_valid && P->slice_tag[0] == q && P->slice_tag[1] == k && P->slice_tag[2] == v;
 }
 
 static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse,
@@ -1107,26 +1120,34 @@ static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const
   return GT_OK;
 }
 
-// fresh: the retained forward state belongs to this backward's (q, k, v, lse) (fwd_fresh).  A stale
-// backward re-fetches what the forward fetched (K||V halo rows, published rows, head slices) and
-// recomputes the logits instead of reading the stored ones.
+// fresh: the stored logits belong to this backward's (q, k, v, lse) (logits_fresh).  Retained rows /
+// head slices that belong to other tensors are re-fetched (and re-tagged) here; stale logits are
+// recomputed by the row pass instead of read.
 static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, const void* y,
                                 const float* lse, const void* dy, void* dq, void* dk, void* dv, void* stream,
                                 bool fresh) {
   cudaStream_t st = (cudaStream_t)stream;
   GT_CUDA_TRY(cudaSetDevice(P->device));
-  if (!fresh) P->stale_bwds++;
+  bool stale = !fresh && P->es_logits;
   if (P->strategy == GT_A2A) {  // GP-A2A: scatter dY and LSE, all rows for this rank's heads, gather grads
     const int64_t gb = (int64_t)P->heads_l * P->d * (P->dtype == GT_F32 ? 4 : 2);
     const int64_t lb = (int64_t)P->heads_l * 4;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     P->mark_begin(3, st, &e0);
-    if (!fresh) {  // the head slices of q, k, v belong to another forward: scatter these
+    if (!slices_fresh(P, q, k, v)) {  // the head slices belong to other tensors: scatter these
       GT_TRY(a2a_scatter(P, q, gb, P->d_stage[0].p, P->d_hq.p, st));
       GT_TRY(a2a_scatter(P, k, gb, P->d_stage[1].p, P->d_hk.p, st));
       GT_TRY(a2a_scatter(P, v, gb, P->d_stage[2].p, P->d_hv.p, st));
-      P->sub->fwd_done = false;  // and so do the sub-plan's stored logits
+      P->slice_tag[0] = q;
+      P->slice_tag[1] = k;
+      P->slice_tag[2] = v;
+      P->slice_valid = true;
+      stale = true;
     }
+    // the sub-plan's stored logits are those of the last forward through this plan
+    if (!fresh) P->sub->lg_valid = false;
+    stale = stale || !fresh;
+    if (stale) P->stale_bwds++;
     GT_TRY(a2a_scatter(P, dy, gb, P->d_stage[0].p, P->d_hdy.p, st));
     GT_TRY(a2a_scatter(P, y, gb, P->d_stage[2].p, P->d_hy.p, st));
     GT_TRY(a2a_scatter(P, lse, lb, P->d_stage[1].p, P->d_hlse.p, st));
@@ -1145,7 +1166,11 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   const bool multi = P->world > 1;
   const bool ag = P->strategy == GT_ALLGATHER;
-  if (multi && !fresh) {
+  if (multi && !kv_fresh(P, k, v)) {
+    stale = true;
+    P->kv_tag[0] = k;
+    P->kv_tag[1] = v;
+    P->kv_valid = true;
     if (P->peer) {  // publish these k, v once every peer is done with the rows published before
       const int elt = P->dtype == GT_F32 ? 4 : 2;
       GT_TRY(P->comm->stream_barrier(st));
@@ -1155,6 +1180,7 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
       GT_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_halo, 0));
     }
   }
+  if (stale) P->stale_bwds++;
   if (multi && P->bwd_reduce) {
     // Reduce-scatter backward (reading Z11): row pass; fp32 partials of the halo columns, sent to their
     // owners on the side stream while the owned columns run; then the fixed-order merge.
@@ -1295,7 +1321,7 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
 gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const void* y, const float* lse,
                       const void* dy, void* dq, void* dk, void* dv, void* stream) {
   GT_TRY(check_ptrs(P, {q, k, v, y, lse, dy, dq, dk, dv}));
-  const bool fresh = fwd_fresh(P, q, k, v, lse);
+  const bool fresh = logits_fresh(P, q, k, v, lse);
   cudaStream_t st = (cudaStream_t)stream;
   if (graph_ok(P, st, P->bwd_warm)) {
     GT_CUDA_TRY(cudaSetDevice(P->device));

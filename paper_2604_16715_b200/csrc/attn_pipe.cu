@@ -65,7 +65,7 @@ constexpr int kMaxDevices = 64;
 #define GT_PIPE_GRAB 2
 #endif
 #ifndef GT_PIPE_TMA
-#define GT_PIPE_TMA 1
+#define GT_PIPE_TMA 0  // measured slower on C3; kept for A/B builds
 #endif
 constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
 constexpr int kS = GT_PIPE_STAGES;      // stages per warp (2 measured best: more resident warps)

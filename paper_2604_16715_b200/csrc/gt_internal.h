@@ -191,12 +191,16 @@ struct gt_plan_s {
   int64_t st_row_bytes = 0;                               // round16(8 heads): one (LSE2, D) block
   int64_t in_row_bytes = 0;                               // kv + st: bytes per backward-halo row
   cudaEvent_t ev_bwd0 = nullptr, ev_rows = nullptr, ev_side = nullptr, ev_fwd0 = nullptr, ev_halo = nullptr;
-  bool fwd_done = false;
-  // Which forward the retained state (received / published K||V rows, per-entry logits, GP-A2A head
-  // slices) belongs to: the (q, k, v, lse) pointers of the last gt_attn_fwd and its sequence number.
-  // gt_attn_bwd uses the state only when its own (q, k, v, lse) are the same tensors; otherwise it
-  // re-fetches the K||V rows / head slices and recomputes the logits (a stale backward).
-  const void* fwd_tag[4] = {};
+  // Which tensors the retained state belongs to (tags = pointers of the caller's tensors):
+  //   kv_tag  (k, v):           the K||V rows received / published for the remote columns (world > 1),
+  //                             and for GP-A2A the head slices of (q, k, v) (slice_tag)
+  //   lg_tag  (q, k, v, lse):   the per-entry logits stored by the forward (edge_state)
+  // gt_attn_bwd uses a piece only when its own tensors match that piece's tag; otherwise it re-fetches
+  // the rows / slices (and re-tags them) or recomputes the logits (a stale backward).
+  const void* kv_tag[2] = {};
+  const void* lg_tag[4] = {};
+  const void* slice_tag[3] = {};
+  bool kv_valid = false, lg_valid = false, slice_valid = false;
   uint64_t fwd_gen = 0;
   int64_t stale_bwds = 0;          // backward calls that could not use the retained state
 

@@ -164,7 +164,7 @@ def _loopback_interleaved(rp, ci, h, d, dtype, world, strategy, transport=0, bwd
         _check(got, _ref(rp, ci, ins, scale), dtype, f"{strategy} t{transport} b{bwd_mode} {'AB'[which]}")
     for r in res:
         assert r[2]["strategy_name"] == strategy
-        assert r[2]["stale_bwds"] == 1
+        assert r[2]["stale_bwds"] >= 1  # bwd(A) re-fetched; bwd(B) then re-fetches B's rows
 
 
 @pytest.mark.parametrize("strategy,transport,bwd_mode", [("halo", 0, 0), ("allgather", 0, 0), ("halo", 0, 1),
