@@ -64,6 +64,9 @@ constexpr int kMaxDevices = 64;
 #ifndef GT_PIPE_GRAB
 #define GT_PIPE_GRAB 2
 #endif
+#ifndef GT_RT_STRIDE
+#define GT_RT_STRIDE 1
+#endif
 #ifndef GT_PIPE_TMA
 #define GT_PIPE_TMA 0  // measured slower on C3; kept for A/B builds
 #endif
@@ -230,6 +233,9 @@ struct PArgs {
                          // bf16 plans, f32x2 for f32 plans), both in local CSR entry order
   const float* es_in;    // rowb: s2 | colb: (P, dS)
   const int32_t* src;    // colb: local CSC position -> local CSR entry (read through a window like nbr)
+  uint32_t rb, rb2, sb;  // row strides (bytes) of the gathered tables as run-time values: a row address is
+                         // then one IMAD.WIDE.U32 (an immediate power-of-two stride becomes shift + high +
+                         // two 64-bit adds)
 };
 
 // lane slice copy of one row: LB bytes at byte offset lane * LB
@@ -564,6 +570,11 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
   const char* const gs_l = PASS == 2 ? a.gs + lane * 16 : nullptr;
   const char* const hs_l = (PASS == 2 && HALO) ? a.halo_s + lane * 16 : nullptr;
   const uint32_t n_loc = (uint32_t)a.n_local;
+#if GT_RT_STRIDE
+  const uint32_t sRB = a.rb, sRB2 = a.rb2, sSB = a.sb;
+#else
+  constexpr uint32_t sRB = RB, sRB2 = 2 * RB, sSB = C::SB;
+#endif
 
   auto finalize_empty = [&](int64_t r) {  // a row (column) with no entries
     float z[EPL];
@@ -691,19 +702,19 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         if (a.peer_shift) {  // NVLink peer load of the owner's published row (kernel param: uniform)
           const uint32_t slot = cv - n_loc;
           const uint32_t own = (slot >> a.peer_shift) & 7, off = slot & ((1u << a.peer_shift) - 1);
-          hrow = row_addr(a.peer[own] + lane * LB, off, 2 * RB);
+          hrow = row_addr(a.peer[own] + lane * LB, off, sRB2);
           if constexpr (PASS == 2) srow = row_addr(a.peer_s[own] + lane * 16, off, C::SB);
         } else {
-          hrow = row_addr(h_l, cv - n_loc, 2 * RB);
+          hrow = row_addr(h_l, cv - n_loc, sRB2);
           if constexpr (PASS == 2) srow = row_addr(hs_l, cv - n_loc, C::SB);
         }
-        pa = loc ? row_addr(ga_l, cv, RB) : hrow;
-        pb = loc ? row_addr(gb_l, cv, RB) : hrow + RB;
-        if constexpr (PASS == 2) ps = loc ? row_addr(gs_l, cv, C::SB) : srow;
+        pa = loc ? row_addr(ga_l, cv, sRB) : hrow;
+        pb = loc ? row_addr(gb_l, cv, sRB) : hrow + RB;
+        if constexpr (PASS == 2) ps = loc ? row_addr(gs_l, cv, sSB) : srow;
       } else {
-        pa = row_addr(ga_l, cv, RB);
-        pb = row_addr(gb_l, cv, RB);
-        if constexpr (PASS == 2) ps = row_addr(gs_l, cv, C::SB);
+        pa = row_addr(ga_l, cv, sRB);
+        pb = row_addr(gb_l, cv, sRB);
+        if constexpr (PASS == 2) ps = row_addr(gs_l, cv, sSB);
       }
       char* dst = st + u * EB + lane * LB;
       cp_lane_z<LB>(dst, pa, valid);
@@ -1215,6 +1226,9 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.qscale = P->scale * pipe::kLog2e;
   a.scale = P->scale;
   a.peer_shift = (P->peer && halo) ? P->peer_shift : 0;
+  a.rb = (uint32_t)((int64_t)P->heads * P->d * (P->dtype == GT_F32 ? 4 : 2));
+  a.rb2 = 2 * a.rb;
+  a.sb = (uint32_t)P->st_row_bytes;
   for (int s = 0; s < 8; ++s) {
     a.peer[s] = (const char*)(pass < 2 ? P->peer_base[s] : P->peer_qd[s]);
     a.peer_s[s] = (const char*)P->peer_st[s];
