@@ -71,6 +71,143 @@ def alg_bytes(h, d, elt):
     }
 
 
+def compulsory_bytes(info, h, d, elt):
+    """Perfect-reuse bytes of each pass (SURVEY.md 8(d) "compulsory bound"): every N-row tensor the pass
+    reads or writes once, the index arrays once, and the entry state it actually reads and writes
+    (gt_plan_info edge_state: base-2 logits f32 [nnz][h] forward -> row pass, (P, dS) [nnz][h] row pass
+    -> column pass, 4 B per head and entry for bf16 plans, 8 B for fp32 plans, read by the column pass
+    through the int32 CSC -> CSR map)."""
+    N, E, Ein = info["n_local"], info["nnz_local"], info["nnz_in_local"]
+    row = N * h * d * elt
+    es = info["edge_state"] == 1
+    s2 = E * h * 4 if es else 0
+    pd = E * h * (4 if elt == 2 else 8) if es else 0
+    item = 20 * N                                  # work-item tables (begin, end, owner) per row
+    return {
+        "fwd": 3 * row + row + N * h * 4 + 4 * E + item + s2,                       # q k v in, y lse out, s2 out
+        "bwd_rows": 4 * row + N * h * 4 + row + N * 8 * h + 4 * E + item + s2 + pd,  # k v dy y lse in, dq D out
+        "bwd_cols": 2 * row + 2 * row + 4 * Ein + item + (4 * Ein + pd if es else N * 8 * h),
+    }
+
+
+def ncu_record(cfg_name, stage):
+    """The committed ncu counters of this pass (profiles/ncu_traffic.json, tools/make_traffic.py) and
+    whether they were taken from the kernel sources in this tree."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(cfg_name, {}).get(stage)
+    except Exception:
+        return None, None
+    if not isinstance(rec, dict):
+        return None, None
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from make_traffic import kernel_sha
+        current = rec.get("kernel_sha") == kernel_sha()
+    except Exception:
+        current = None
+    return rec, current
+
+
+def l2_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_bw.json")) as f:
+            return float(json.load(f)["l2_read_gbs"])
+    except Exception:
+        return None
+
+
+def physical_roofline(cfg, dom, stage_ms, per, units, comp, peak, peak_src):
+    """The dominant pass against the HBM roofline, physically: DRAM bytes ncu measured for this kernel
+    (per launch, cold cache, profiles/ncu_traffic.json) over its live CUDA-event launch time, as a
+    fraction of the measured HBM peak; this cannot exceed 1 by construction.  Next
+    to it: the two algorithmic models (no-reuse gather model of SURVEY 8(d), an upper bound on traffic
+    that L2 reuse beats on community graphs, and the perfect-reuse compulsory bytes, a lower bound), the
+    L2 roofline (lts bytes over the measured L2 read bandwidth, profiles/l2_bw.json) and the resource
+    whose ncu utilisation is highest ("binding")."""
+    t = stage_ms[dom] * 1e-3
+    gather = per[dom][0] * units[dom][0] + per[dom][1] * units[dom][1]
+    rec, current = ncu_record(cfg.name, dom)
+    dram = rec["dram_bytes"] if rec else None
+    out = {"bound": "hbm", "kernel": dom, "launch_ms": stage_ms[dom], "peak": peak, "unit": "GB/s",
+           "peak_source": peak_src,
+           "achieved": dram / t / 1e9 if dram else None,
+           "frac": dram / t / 1e9 / peak if dram else None,
+           "achieved_basis": "ncu DRAM bytes (read + write) of this kernel per launch / its live launch time",
+           "traffic": dram, "traffic_kernel_sha_current": current,
+           "models": {
+               "gather_no_reuse": {"bytes": gather, "gbs": gather / t / 1e9, "frac": gather / t / 1e9 / peak,
+                                   "note": "SURVEY 8(d) no-reuse gather model: every gathered row from HBM; "
+                                           "a model, not a roofline fraction, when L2 reuse beats it (> 1)"},
+               "compulsory": {"bytes": comp[dom], "gbs": comp[dom] / t / 1e9, "frac": comp[dom] / t / 1e9 / peak,
+                              "note": "perfect reuse: each N-row tensor, index array and entry-state array once"}},
+           "all_passes": {}}
+    l2p = l2_peak()
+    for s_, ms_ in stage_ms.items():
+        r, _ = ncu_record(cfg.name, s_)
+        e = {"ms": ms_, "compulsory_frac": comp[s_] / (ms_ * 1e-3) / 1e9 / peak}
+        if r:
+            e["dram_frac"] = r["dram_bytes"] / (ms_ * 1e-3) / 1e9 / peak
+            if r.get("l2_bytes") and l2p:
+                e["l2_frac"] = r["l2_bytes"] / (ms_ * 1e-3) / 1e9 / l2p
+            e["util_pct"] = {k: r.get(k) for k in ("issue_active_pct", "dram_pct", "l2_pct", "l1_pct")}
+        out["all_passes"][s_] = e
+    if rec:
+        util = {"issue": rec.get("issue_active_pct"), "dram": rec.get("dram_pct"), "l2": rec.get("l2_pct"),
+                "l1": rec.get("l1_pct")}
+        out["util_pct"] = {k: v for k, v in util.items() if v is not None}
+        if rec.get("l2_bytes") and l2p:
+            out["l2"] = {"bytes": rec["l2_bytes"], "achieved": rec["l2_bytes"] / t / 1e9, "peak": l2p,
+                         "frac": rec["l2_bytes"] / t / 1e9 / l2p, "unit": "GB/s",
+                         "peak_source": "profiles/l2_bw.json (tools/l2bw.cu, L2 -> SM read bandwidth)"}
+        # the resource closest to its limit: DRAM and L2 bytes against their measured peaks, issue slots
+        # against 100 % (ncu smsp__issue_active)
+        cand = {"hbm": out["frac"], "l2": out.get("l2", {}).get("frac"),
+                "issue": (rec["issue_active_pct"] / 100.0) if rec.get("issue_active_pct") else None}
+        cand = {k: v for k, v in cand.items() if v is not None}
+        out["binding"] = max(cand, key=cand.get) if cand else None
+        out["binding_fracs"] = cand
+        if rec.get("inst"):
+            out["warp_inst_per_entry"] = rec["inst"] / max(units[dom][0], 1)
+    return out
+
+
+def step_dram_frac(cfg, ms, peak):
+    tot = 0.0
+    for s_ in ("fwd", "bwd_rows", "bwd_cols"):
+        r, _ = ncu_record(cfg.name, s_)
+        if not r:
+            return None
+        tot += r["dram_bytes"]
+    return tot / (ms * 1e-3) / 1e9 / peak
+
+
+def bitexact_partition_halo(gt, rp, ci, worlds=(2, 4, 8)):
+    """SURVEY 8(d) report field: libgt's host partition and halo sets (gt_partition, gt_halo) against
+    the oracle's (linear scan, mark arrays) on the bench graph, bit for bit."""
+    import numpy as np
+    import oracle
+    ok = True
+    for p in worlds:
+        b = gt.partition(rp, p)
+        ok &= bool(np.array_equal(b, oracle.partition(rp, p)))
+        for r in range(p):
+            for inward in (False, True):
+                ok &= bool(np.array_equal(gt.halo(rp, ci, int(b[r]), int(b[r + 1]), inward),
+                                          oracle.halo(rp, ci, int(b[r]), int(b[r + 1]), inward)))
+    return ok
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 class Clocks:
     """Samples nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -135,8 +272,10 @@ def report_fields(per_step, stages, info, world, nnz, step_bytes, peak):
         "t_fwd_ms": stages["fwd"][0] / nsteps if "fwd" in stages else None,
         "t_bwd_ms": (stages["bwd_rows"][0] + stages["bwd_cols"][0]) / nsteps,
         "edges_per_s_per_gpu": nnz / (mean * 1e-3) / world,
-        "B_alg_bytes": step_bytes, "hbm_frac_measured_peak": step_bytes / (mean * 1e-3) / 1e9 / peak,
-        "hbm_frac_8000": step_bytes / (mean * 1e-3) / 8e12,
+        "B_alg_bytes_gather_model": step_bytes,
+        "gather_model_frac_measured_peak": step_bytes / (mean * 1e-3) / 1e9 / peak,
+        "gather_model_frac_8000": step_bytes / (mean * 1e-3) / 8e12,
+        "parallel_eff": None,  # T(1) / (p T(p)): computed by the driver from the per-N runs
         "exch_bytes_per_rank": exch_bytes, "t_exch_ms": t_exch,
         "nvlink_frac": (exch_bytes / (t_exch * 1e-3) / 900e9) if t_exch > 0 else None,
         "gpu_name": torch.cuda.get_device_name(), "torch_cuda": torch.version.cuda,
@@ -237,7 +376,8 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name} (oracle sample)", "nodes": len(rp) - 1, "nnz": int(len(ci)),
                        "heads": cfg.heads, "head_dim": cfg.d, "input_dtype": cfg.dtype},
-            "cpu_baseline": {"value": val, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": val, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -330,28 +470,14 @@ def run_ours(args):
         ms = float(t.item())
 
     # ---- roofline of the dominant kernel stage (per launch, device-timed on the launching stream) ----
+    stage_ms = {s: (stages[s][0] / max(stages[s][1], 1)) for s in ("fwd", "bwd_rows", "bwd_cols")}
+    dom = max(stage_ms, key=stage_ms.get)
     per = alg_bytes(h, d, elt)
     units = {"fwd": (info["nnz_local"], info["n_local"]), "bwd_rows": (info["nnz_local"], info["n_local"]),
              "bwd_cols": (info["nnz_in_local"], info["n_local"])}
-    stage_ms = {s: (stages[s][0] / max(stages[s][1], 1)) for s in ("fwd", "bwd_rows", "bwd_cols")}
-    dom = max(stage_ms, key=stage_ms.get)
-    dom_bytes = per[dom][0] * units[dom][0] + per[dom][1] * units[dom][1]
     peak, peak_src = peaks()
-    achieved = dom_bytes / (stage_ms[dom] * 1e-3) / 1e9
     step_bytes = sum(per[s][0] * units[s][0] + per[s][1] * units[s][1] for s in per)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(cfg.name, {}).get(dom)
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "alg_bytes_per_launch": dom_bytes, "launch_ms": stage_ms[dom],
-                # the DRAM bytes ncu measured for this kernel (profiles/, cold cache) over its live launch
-                # time: real HBM utilisation, as opposed to the no-reuse algorithmic model above
-                "dram_achieved": (traffic / (stage_ms[dom] * 1e-3) / 1e9) if traffic else None,
-                "dram_frac": (traffic / (stage_ms[dom] * 1e-3) / 1e9 / peak) if traffic else None}
+    roofline = physical_roofline(cfg, dom, stage_ms, per, units, compulsory_bytes(info, h, d, elt), peak, peak_src)
 
     # ---- end to end through the C ABI with pinned host buffers ----
     e2e = None
@@ -382,14 +508,23 @@ def run_ours(args):
         sub_rp, sub_ci, R = induced_prefix_subgraph(rp, ci, target)
         tc, feats, refs = oracle_step(sub_rp, sub_ci, R, cfg, 9, scale, keep=True)
         cpu = {"value": float(sub_rp[-1]) / tc, "unit": "edges/s", "cores": gtgen.num_threads(), "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"fp64 oracle fwd+bwd on the subgraph induced by the first {R} nodes "
                          f"({int(sub_rp[-1])} entries), {tc:.1f} s",
                # the CUDA path on the same sample and inputs against these oracle results
                "parity_normwise": sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs)}
         del feats, refs
+        t_bx = time.perf_counter()
+        cpu["bitexact_partition_halo"] = bitexact_partition_halo(gt, rp, ci)
+        cpu["bitexact_check_s"] = time.perf_counter() - t_bx
 
     if rank == 0:
         value = nnz / (ms * 1e-3)
+        rep = report_fields(per_step, stages, info, world, nnz, step_bytes, peak)
+        if cpu:
+            rep["max_rel_err"] = cpu["parity_normwise"]
+            rep["bitexact_partition_halo"] = cpu["bitexact_partition_halo"]
+            rep["oracle_threads"], rep["oracle_cpu"] = cpu["cores"], cpu["cpu_model"]
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -402,7 +537,10 @@ def run_ours(args):
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
                        "bwd_mode": info["bwd_mode"], "transport": info["transport"]},
             "roofline": roofline,
-            "step_hbm_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
+            # whole step: ncu DRAM bytes of the three passes over the step time (physical), and the
+            # no-reuse gather model (exceeds 1 on L2-local graphs: a model, not a fraction of the peak)
+            "step_dram_frac": step_dram_frac(cfg, ms, peak),
+            "step_gather_model_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
             "stages_ms": {s: stages[s][0] / max(stages[s][1], 1) for s in stages},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": (info["launches_fwd"] + info["launches_bwd"]) * args.steps,
@@ -411,7 +549,7 @@ def run_ours(args):
                      "heavy_cols": info["heavy_cols"], "exch_fwd_bytes": info["exch_fwd_bytes"],
                      "exch_bwd_bytes": info["exch_bwd_bytes"], "predicted_ms": info["predicted_ms"]},
             # SURVEY 8(d) report fields (rank 0's view; step times are this rank's CUDA events)
-            "report": report_fields(per_step, stages, info, world, nnz, step_bytes, peak),
+            "report": rep,
         }
         print(json.dumps(line), flush=True)
     plan.close()

@@ -59,6 +59,7 @@ extern "C" {
 
 typedef struct gt_plan_s* gt_plan_t;     /* opaque; owned by the library, released by gt_free */
 typedef struct gt_loopback_s* gt_loopback_t; /* opaque in-process multi-rank group (tests) */
+typedef struct gt_hostipc_s* gt_hostipc_t;   /* opaque host-bootstrapped CUDA-IPC group (one process per rank) */
 
 typedef enum {
   GT_OK = 0,
@@ -89,8 +90,11 @@ typedef enum {
 typedef enum {
   GT_COMM_NONE = 0,     /* world == 1 */
   GT_COMM_NCCL = 1,     /* comm = ncclComm_t (from gt_nccl_comm_create), one process per GPU */
-  GT_COMM_LOOPBACK = 2  /* comm = gt_loopback_t; all ranks are host threads of one process on
+  GT_COMM_LOOPBACK = 2, /* comm = gt_loopback_t; all ranks are host threads of one process on
                            devices that can address each other (tests on a single GPU) */
+  GT_COMM_HOSTIPC = 3   /* comm = gt_hostipc_t (gt_hostipc_create); one process per rank, devices that can
+                           map each other's allocations with CUDA IPC (several processes on one GPU, or
+                           GPUs of one node); host collectives through caller callbacks (e.g. gloo) */
 } gt_comm_kind;
 
 /* Host CSR of the GLOBAL graph, identical on every rank; borrowed for the duration of gt_plan.
@@ -104,7 +108,7 @@ typedef struct {
 typedef struct {
   int rank;                /* this rank, 0 <= rank < world */
   int comm_kind;           /* gt_comm_kind */
-  void* comm;              /* ncclComm_t or gt_loopback_t, borrowed; NULL iff world == 1 */
+  void* comm;              /* ncclComm_t, gt_loopback_t or gt_hostipc_t, borrowed; NULL iff world == 1 */
   int dtype;               /* gt_dtype of q, k, v, y, dy, dq, dk, dv */
   float scale;             /* multiplier of Q K^T; 0 => 1/sqrt(heads * d) */
   int strategy;            /* gt_strategy */
@@ -272,6 +276,22 @@ void gt_nccl_comm_destroy(void* comm);
  * device-to-device on the caller's streams).  Used to test the multi-rank path on one GPU. */
 gt_status gt_loopback_create(int world, gt_loopback_t* out);
 void gt_loopback_destroy(gt_loopback_t g);
+
+/* Host-bootstrapped CUDA-IPC group (GT_COMM_HOSTIPC): one process per rank, device current at
+ * creation.  Device data moves as in Alg. 1 - all-to-all-v of packed rows, all-gather -
+ * by CUDA IPC: the sender publishes the IPC handle of the allocation holding its rows and an
+ * interprocess event recorded after they were written; receivers wait on the event on their stream
+ * and copy out of the mapped allocation; senders wait on the receivers' "done" events before reusing
+ * their rows.  Host collectives go through coll->allgather(ctx, send, recv, bytes): every rank passes
+ * `bytes` bytes, recv[world * bytes] receives them in rank order; host-synchronous; 0 = success
+ * (anything else => GT_ENCCL).  gt_hostipc_create is collective; the callback must stay valid until
+ * gt_hostipc_destroy, which must follow gt_free of every plan using the group. */
+typedef struct {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes);
+} gt_host_coll;
+gt_status gt_hostipc_create(const gt_host_coll* coll, int world, int rank, gt_hostipc_t* out);
+void gt_hostipc_destroy(gt_hostipc_t g);
 
 /* ------------------------------------------------------------- host-only planning helpers -- */
 /* Row partition (reading Z9): mode 0 => bounds[r] = min{ i : row_ptr[i] + i >= ceil(r (nnz + n) / p) },

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
@@ -60,7 +60,9 @@ def _dt(x: np.ndarray) -> int:
         return F32
     if x.dtype == np.uint16:
         return BF16
-    raise TypeError(f"oracle inputs are float32 or bf16 bits (uint16), got {x.dtype}")
+    if x.dtype == np.float64:
+        return F64
+    raise TypeError(f"oracle inputs are float32, bf16 bits (uint16) or float64, got {x.dtype}")
 
 
 def _c(x, dtype=None):

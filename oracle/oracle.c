@@ -26,7 +26,7 @@
  * Dataflow (deliberately different from the GPU's): two-pass softmax per row-head
  * (max, then sum), P and dS stored per edge in fp64, dK/dV through the oracle's own
  * counting-sort transpose.  All arithmetic is fp64 on inputs upcast exactly from
- * their storage dtype (fp32 or bf16 bit patterns).
+ * their storage dtype (fp32 or bf16 bit patterns, or fp64 as is).
  *
  * Partition / halo (readings Z9, Z10): contiguous row ranges balancing
  * rows + edges, found by a linear scan; halo sets by mark arrays.
@@ -39,9 +39,12 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { OR_F32 = 0, OR_BF16 = 1 };
+enum { OR_F32 = 0, OR_BF16 = 1, OR_F64 = 2 };
 
+/* fp64 inputs (OR_F64) are read as they are: used by the SGA-block oracle (oracle/sga.py), whose
+ * Q = X W_Q, K, V (Eq. 3) are fp64 products. */
 static inline double ld(const void* x, int dt, int64_t i) {
+  if (dt == OR_F64) return ((const double*)x)[i];
   if (dt == OR_F32) return (double)((const float*)x)[i];
   uint32_t u = (uint32_t)((const uint16_t*)x)[i] << 16;
   float f;

@@ -464,7 +464,8 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     return fail(GT_ECONFIG, "gt_plan: unsupported shape: need heads in {1,2,4,8}, heads*d in {64,128,256,512}, "
                             "dtype f32|bf16; got heads=" + std::to_string(heads) + " d=" + std::to_string(d));
   if (world < 1 || opts->rank < 0 || opts->rank >= world) return fail(GT_EINVAL, "gt_plan: bad world/rank");
-  if (world > 1 && (!opts->comm || (opts->comm_kind != GT_COMM_NCCL && opts->comm_kind != GT_COMM_LOOPBACK)))
+  if (world > 1 && (!opts->comm || (opts->comm_kind != GT_COMM_NCCL && opts->comm_kind != GT_COMM_LOOPBACK &&
+                                    opts->comm_kind != GT_COMM_HOSTIPC)))
     return fail(GT_EINVAL, "gt_plan: world > 1 needs a communicator");
   if (opts->strategy < GT_AUTO || opts->strategy > GT_A2A) return fail(GT_EINVAL, "gt_plan: unknown strategy");
   if (world == 1 && (opts->strategy == GT_ALLGATHER || opts->strategy == GT_HALO || opts->strategy == GT_A2A))
@@ -506,8 +507,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
 
   gt_status cst = GT_OK;
   if (world > 1) {
-    P->comm = opts->comm_kind == GT_COMM_NCCL ? make_nccl_comm(opts->comm, world, opts->rank, &cst)
-                                               : make_loopback_comm((gt_loopback_t)opts->comm, world, opts->rank, &cst);
+    P->comm = opts->comm_kind == GT_COMM_NCCL       ? make_nccl_comm(opts->comm, world, opts->rank, &cst)
+              : opts->comm_kind == GT_COMM_HOSTIPC ? make_hostipc_comm((gt_hostipc_t)opts->comm, world, opts->rank, &cst)
+                                                   : make_loopback_comm((gt_loopback_t)opts->comm, world, opts->rank, &cst);
     if (!P->comm) return cst;
   }
 

@@ -513,8 +513,14 @@ struct Meta {      // warp-uniform description of one filled stage
 #ifndef GT_COLB_MINB
 #define GT_COLB_MINB 1
 #endif
+#ifndef GT_FWD_MINB
+#define GT_FWD_MINB 1
+#endif
+#ifndef GT_CARVEOUT  // preferred shared-memory carveout (percent of the unified L1/shared array); -1 = driver's
+#define GT_CARVEOUT -1
+#endif
 template <int PASS, int ES, int EPL>
-constexpr int min_ctas() { return EPL > 8 ? 1 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : 1)); }
+constexpr int min_ctas() { return EPL > 8 ? 1 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : GT_FWD_MINB)); }
 
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
 __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
@@ -1115,6 +1121,8 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
     if (!grid_of[dev]) {
       auto k = pipe_kernel<T, H, D, PASS, HALO, ES>;
       GT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if (GT_CARVEOUT >= 0)
+        GT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, GT_CARVEOUT));
       int per = 0;
       GT_CUDA_TRY(cudaDeviceGetAttribute(&sms_of[dev], cudaDevAttrMultiProcessorCount, dev));
       GT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kWarps * 32, smem));

@@ -1,15 +1,21 @@
-// Exchange layer: pack kernels, NCCL transport (loaded at run time), in-process loopback transport.
+// Exchange layer: pack kernels, NCCL transport (loaded at run time), in-process loopback transport,
+// and the host-bootstrapped CUDA-IPC transport (one process per rank on devices that can map each
+// other's memory, host collectives through caller callbacks, e.g. a gloo process group).
 //
 // Forward exchange (Alg. 1 lines 2 and 5): K||V rows of remote columns, packed
 // [k | v] per row.  Backward exchange (reading Z11, transposed owner), in two messages so the first
 // overlaps the row pass: [q | dy] rows of in-neighbour rows (known at backward entry), then their
 // (LSE2, D) blocks (written by the row pass).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdint.h>
 
 #include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -429,6 +435,224 @@ Comm* make_loopback_comm(gt_loopback_t g, int world, int rank, gt_status* st) {
 
 }  // namespace gt
 
+// ----------------------------------------------------------------- host IPC --
+// One process per rank.  Host collectives (an all-gather of a few bytes) go through the caller's
+// callback; device data moves by CUDA IPC: each rank publishes the IPC handle of the allocation holding
+// its send rows and an interprocess event recorded after they were written; the receivers wait on that
+// event on their own stream and copy straight out of the mapped peer allocation (cudaMemcpyAsync
+// device to device), then every rank waits on the receivers' "done" events before its send rows may be
+// rewritten.  Same protocol as the loopback transport, across processes.
+struct gt_hostipc_s {
+  gt_host_coll coll;
+  int world = 1, rank = 0, device = 0;
+  cudaEvent_t ready = nullptr, done = nullptr;          // this rank's interprocess events
+  std::vector<cudaEvent_t> peer_ready, peer_done;       // opened peer events (own slot: own events)
+  std::map<std::string, void*> opened;                  // peer allocation (handle bytes) -> mapping
+  std::mutex mu;
+  ~gt_hostipc_s() {
+    for (auto& kv : opened) cudaIpcCloseMemHandle(kv.second);
+    for (int s = 0; s < world; ++s)
+      if (s != rank) {
+        if (s < (int)peer_ready.size() && peer_ready[s]) cudaEventDestroy(peer_ready[s]);
+        if (s < (int)peer_done.size() && peer_done[s]) cudaEventDestroy(peer_done[s]);
+      }
+    if (ready) cudaEventDestroy(ready);
+    if (done) cudaEventDestroy(done);
+  }
+  gt_status allgather(const void* send, void* recv, int64_t bytes) {
+    if (coll.allgather(coll.ctx, send, recv, bytes) != 0)
+      return gt::fail(GT_ENCCL, "host IPC: the host all-gather callback failed");
+    return GT_OK;
+  }
+  gt_status barrier() {
+    char x = 0;
+    std::vector<char> all((size_t)world);
+    return allgather(&x, all.data(), 1);
+  }
+};
+
+namespace gt {
+namespace {
+
+// base of the allocation holding p and p's offset in it (cudaIpcGetMemHandle needs the base)
+gt_status alloc_base(const void* p, char** base, int64_t* off) {
+  static PFN_cuMemGetAddressRange_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(f);
+  });
+  if (!fn) return fail(GT_ECUDA, "cuMemGetAddressRange is not available");
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return fail(GT_ECUDA, "host IPC: not a device allocation");
+  *base = (char*)b;
+  *off = (int64_t)((const char*)p - (const char*)b);
+  return GT_OK;
+}
+
+struct IpcRef {            // one rank's published buffer
+  cudaIpcMemHandle_t h;
+  int64_t off;
+};
+
+gt_status publish(gt_hostipc_s* g, const void* p, std::vector<IpcRef>& all, bool has) {
+  IpcRef mine;
+  std::memset(&mine, 0, sizeof(mine));
+  if (has) {
+    char* base = nullptr;
+    GT_TRY(alloc_base(p, &base, &mine.off));
+    GT_CUDA_TRY(cudaIpcGetMemHandle(&mine.h, base));
+  } else {
+    mine.off = -1;
+  }
+  all.resize((size_t)g->world);
+  return g->allgather(&mine, all.data(), sizeof(mine));
+}
+
+gt_status open_ref(gt_hostipc_s* g, const IpcRef& ref, char** out) {
+  std::string key((const char*)&ref.h, sizeof(ref.h));
+  auto it = g->opened.find(key);
+  if (it == g->opened.end()) {
+    void* p = nullptr;
+    GT_CUDA_TRY(cudaIpcOpenMemHandle(&p, ref.h, cudaIpcMemLazyEnablePeerAccess));
+    it = g->opened.emplace(key, p).first;
+  }
+  *out = (char*)it->second + ref.off;
+  return GT_OK;
+}
+
+struct HostIpcComm : Comm {
+  gt_hostipc_s* g;
+  explicit HostIpcComm(gt_hostipc_s* g_) : g(g_) {}
+  int world() const override { return g->world; }
+  int rank() const override { return g->rank; }
+  // every rank records `done` after its receives, then waits on every peer's `done` (its own send rows
+  // may only be rewritten after all readers copied them); the final barrier keeps events from being
+  // re-recorded before every rank has enqueued its waits
+  gt_status finish(cudaStream_t stream, gt_status st) {
+    if (cudaEventRecord(g->done, stream) != cudaSuccess && st == GT_OK) st = fail(GT_ECUDA, "host IPC: record");
+    gt_status b = g->barrier();
+    if (b != GT_OK) return b;
+    for (int s = 0; s < g->world; ++s)
+      if (s != g->rank && cudaStreamWaitEvent(stream, g->peer_done[s], 0) != cudaSuccess && st == GT_OK)
+        st = fail(GT_ECUDA, "host IPC: wait");
+    b = g->barrier();
+    return b != GT_OK ? b : st;
+  }
+  gt_status exchange(const void* send_buf, const int64_t* send_off, const int64_t* send_cnt, void* recv_buf,
+                     const int64_t* recv_off, const int64_t* recv_cnt, int64_t row_bytes,
+                     cudaStream_t stream) override {
+    std::lock_guard<std::mutex> lock(g->mu);
+    const int w = g->world, r = g->rank;
+    int64_t nsend = 0;
+    for (int s = 0; s < w; ++s)
+      if (s != r) nsend += send_cnt[s];
+    GT_CUDA_TRY(cudaEventRecord(g->ready, stream));
+    std::vector<IpcRef> refs;
+    GT_TRY(publish(g, send_buf, refs, nsend > 0 && send_buf));
+    // protocol record: row size and this rank's (offset, count) per destination
+    std::vector<int64_t> mine(1 + 2 * (size_t)w), all((size_t)w * (1 + 2 * (size_t)w));
+    mine[0] = row_bytes;
+    for (int s = 0; s < w; ++s) { mine[1 + 2 * s] = send_off[s]; mine[2 + 2 * s] = send_cnt[s]; }
+    GT_TRY(g->allgather(mine.data(), all.data(), (int64_t)(mine.size() * sizeof(int64_t))));
+    gt_status st = GT_OK;
+    for (int s = 0; s < w && st == GT_OK; ++s) {
+      if (s == r) continue;
+      const int64_t* pr = all.data() + (size_t)s * (1 + 2 * w);
+      if (pr[0] != row_bytes || pr[2 + 2 * r] != recv_cnt[s]) {
+        st = fail(GT_ENCCL, "host IPC exchange: protocol mismatch between ranks " + std::to_string(r) + " and " +
+                                std::to_string(s));
+        break;
+      }
+      if (recv_cnt[s] == 0) continue;
+      char* src = nullptr;
+      st = open_ref(g, refs[(size_t)s], &src);
+      if (st != GT_OK) break;
+      if (cudaStreamWaitEvent(stream, g->peer_ready[s], 0) != cudaSuccess ||
+          cudaMemcpyAsync((char*)recv_buf + recv_off[s] * row_bytes, src + pr[1 + 2 * r] * row_bytes,
+                          (size_t)(recv_cnt[s] * row_bytes), cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+        st = fail(GT_ECUDA, "host IPC exchange: copy failed");
+    }
+    return finish(stream, st);
+  }
+  std::vector<int64_t> ag_off, ag_cnt, ag_roff;
+  gt_status all_gather(const void* send_buf, void* recv_buf, int64_t rows, int64_t row_bytes,
+                       cudaStream_t stream) override {
+    const int w = g->world, r = g->rank;
+    ag_off.assign(w, 0);
+    ag_cnt.assign(w, rows);
+    ag_roff.resize(w);
+    for (int s = 0; s < w; ++s) ag_roff[s] = s * rows;
+    if (rows > 0)
+      GT_CUDA_TRY(cudaMemcpyAsync((char*)recv_buf + r * rows * row_bytes, send_buf, (size_t)(rows * row_bytes),
+                                  cudaMemcpyDeviceToDevice, stream));
+    return exchange(send_buf, ag_off.data(), ag_cnt.data(), recv_buf, ag_roff.data(), ag_cnt.data(), row_bytes,
+                    stream);
+  }
+  gt_status broadcast_host(void* data, int64_t bytes, cudaStream_t) override {
+    std::vector<char> all((size_t)(bytes * g->world));
+    GT_TRY(g->allgather(data, all.data(), bytes));
+    std::memcpy(data, all.data(), (size_t)bytes);  // rank 0's
+    return GT_OK;
+  }
+  gt_status max_host(double* v, cudaStream_t) override {
+    std::vector<double> all((size_t)g->world);
+    GT_TRY(g->allgather(v, all.data(), sizeof(double)));
+    for (double x : all) *v = std::max(*v, x);
+    return GT_OK;
+  }
+  gt_status barrier(cudaStream_t) override { return g->barrier(); }
+  gt_status stream_barrier(cudaStream_t stream) override {
+    std::lock_guard<std::mutex> lock(g->mu);
+    GT_CUDA_TRY(cudaEventRecord(g->ready, stream));
+    GT_TRY(g->barrier());
+    gt_status st = GT_OK;
+    for (int s = 0; s < g->world; ++s)
+      if (s != g->rank && cudaStreamWaitEvent(stream, g->peer_ready[s], 0) != cudaSuccess)
+        st = fail(GT_ECUDA, "host IPC: stream barrier wait");
+    GT_TRY(g->barrier());
+    return st;
+  }
+  gt_status share_pointers(void* local, void** peers, cudaStream_t) override {
+    std::lock_guard<std::mutex> lock(g->mu);
+    std::vector<IpcRef> refs;
+    GT_TRY(publish(g, local, refs, local != nullptr));
+    for (int s = 0; s < g->world; ++s) {
+      if (s == g->rank || refs[(size_t)s].off < 0) {
+        peers[s] = s == g->rank ? local : nullptr;
+        continue;
+      }
+      char* p = nullptr;
+      GT_TRY(open_ref(g, refs[(size_t)s], &p));
+      peers[s] = p;
+    }
+    return GT_OK;
+  }
+};
+
+}  // namespace
+
+Comm* make_hostipc_comm(gt_hostipc_t g, int world, int rank, gt_status* st) {
+  if (!g || g->world != world || g->rank != rank) {
+    *st = fail(GT_EINVAL, "host IPC group does not match (world, rank)");
+    return nullptr;
+  }
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != g->device) {
+    *st = fail(GT_EINVAL, "host IPC group was created on another device");
+    return nullptr;
+  }
+  *st = GT_OK;
+  return new HostIpcComm(g);
+}
+
+}  // namespace gt
+
 using namespace gt;
 
 extern "C" {
@@ -443,6 +667,40 @@ gt_status gt_loopback_create(int world, gt_loopback_t* out) {
 }
 
 void gt_loopback_destroy(gt_loopback_t g) { delete g; }
+
+gt_status gt_hostipc_create(const gt_host_coll* coll, int world, int rank, gt_hostipc_t* out) {
+  if (!coll || !coll->allgather || !out || world < 1 || rank < 0 || rank >= world)
+    return fail(GT_EINVAL, "gt_hostipc_create: bad arguments");
+  *out = nullptr;
+  auto g = std::make_unique<gt_hostipc_s>();
+  g->coll = *coll;
+  g->world = world;
+  g->rank = rank;
+  GT_CUDA_TRY(cudaGetDevice(&g->device));
+  const unsigned fl = cudaEventDisableTiming | cudaEventInterprocess;
+  GT_CUDA_TRY(cudaEventCreateWithFlags(&g->ready, fl));
+  GT_CUDA_TRY(cudaEventCreateWithFlags(&g->done, fl));
+  cudaIpcEventHandle_t mine[2];
+  GT_CUDA_TRY(cudaIpcGetEventHandle(&mine[0], g->ready));
+  GT_CUDA_TRY(cudaIpcGetEventHandle(&mine[1], g->done));
+  std::vector<cudaIpcEventHandle_t> all((size_t)world * 2);
+  GT_TRY(g->allgather(mine, all.data(), sizeof(mine)));
+  g->peer_ready.assign(world, nullptr);
+  g->peer_done.assign(world, nullptr);
+  for (int s = 0; s < world; ++s) {
+    if (s == rank) {
+      g->peer_ready[s] = g->ready;
+      g->peer_done[s] = g->done;
+      continue;
+    }
+    GT_CUDA_TRY(cudaIpcOpenEventHandle(&g->peer_ready[s], all[2 * (size_t)s]));
+    GT_CUDA_TRY(cudaIpcOpenEventHandle(&g->peer_done[s], all[2 * (size_t)s + 1]));
+  }
+  *out = g.release();
+  return GT_OK;
+}
+
+void gt_hostipc_destroy(gt_hostipc_t g) { delete g; }
 
 gt_status gt_nccl_unique_id(void* uid128) {
   if (!uid128) return fail(GT_EINVAL, "null uid");

@@ -73,6 +73,7 @@ struct Comm {
 
 Comm* make_nccl_comm(void* nccl_comm, int world, int rank, gt_status* st);
 Comm* make_loopback_comm(gt_loopback_t g, int world, int rank, gt_status* st);
+Comm* make_hostipc_comm(gt_hostipc_t g, int world, int rank, gt_status* st);
 
 // ------------------------------------------------------------------- plan --
 struct ChunkTable {        // rows (or columns) split into chunks of <= chunk edges

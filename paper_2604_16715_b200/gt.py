@@ -19,7 +19,7 @@ GT_F32, GT_BF16 = 0, 1
 GT_AUTO, GT_SINGLE, GT_ALLGATHER, GT_HALO = range(4)
 STRATEGIES = {"auto": GT_AUTO, "single": GT_SINGLE, "allgather": GT_ALLGATHER, "halo": GT_HALO, "a2a": 4}
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
-GT_COMM_NONE, GT_COMM_NCCL, GT_COMM_LOOPBACK = range(3)
+GT_COMM_NONE, GT_COMM_NCCL, GT_COMM_LOOPBACK, GT_COMM_HOSTIPC = range(4)
 EXPORT = {"bounds": 0, "halo_out": 1, "halo_in": 2, "send_out": 3, "send_in": 4, "csc_ptr": 5, "csc_idx": 6,
           "heavy_rows": 7, "heavy_cols": 8}
 _EXPORT_I64 = {"bounds", "csc_ptr"}
@@ -114,6 +114,9 @@ def lib():
         L.gt_loopback_create.argtypes = [ctypes.c_int, ctypes.POINTER(_P)]
         L.gt_loopback_destroy.argtypes = [_P]
         L.gt_loopback_destroy.restype = None
+        L.gt_hostipc_create.argtypes = [ctypes.POINTER(_HostColl), ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]
+        L.gt_hostipc_destroy.argtypes = [_P]
+        L.gt_hostipc_destroy.restype = None
         L.gt_partition.argtypes = [_I64, _P, ctypes.c_int, ctypes.c_int, _P]
         L.gt_halo.argtypes = [_I64, _P, _P, _I64, _I64, ctypes.c_int, _P, _I64, ctypes.POINTER(_I64)]
         L.gt_send_list.argtypes = [_I64, _P, _P, _I64, _I64, _I64, _I64, ctypes.c_int, _P, _I64,
@@ -214,6 +217,47 @@ class LoopbackGroup:
             self.handle = None
 
 
+_ALLGATHER_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
+class _HostColl(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allgather", _ALLGATHER_CB)]
+
+
+class HostIpcGroup:
+    """GT_COMM_HOSTIPC: one process per rank, device data moved by CUDA IPC (gt_hostipc_create), host
+    collectives over a torch.distributed process group (gloo): several processes can share ONE GPU,
+    which NCCL refuses.  Create it with the rank's CUDA device current; close it after every plan."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+        def allgather(_ctx, send, recv, nbytes):
+            try:
+                t = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8)
+                out = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(out, t, group=self.group)
+                flat = torch.cat(out).numpy()
+                ctypes.memmove(recv, flat.ctypes.data, self.world * nbytes)
+                return 0
+            except Exception:  # reported to the library as a failed collective (GT_ENCCL)
+                return 1
+
+        self._cb = _ALLGATHER_CB(allgather)      # kept alive as long as the group
+        self._coll = _HostColl(None, self._cb)
+        h = _P()
+        _check(lib().gt_hostipc_create(ctypes.byref(self._coll), self.world, self.rank, ctypes.byref(h)))
+        self.handle = h.value
+
+    def close(self):
+        if self.handle:
+            lib().gt_hostipc_destroy(self.handle)
+            self.handle = None
+
+
 class NcclComm:
     """NCCL communicator bootstrapped over a torch.distributed process group (rank 0's unique id is
     broadcast through the group)."""
@@ -304,8 +348,10 @@ class Plan:
                 opts.comm_kind, opts.comm = GT_COMM_LOOPBACK, comm.handle
             elif isinstance(comm, NcclComm):
                 opts.comm_kind, opts.comm = GT_COMM_NCCL, comm.handle
+            elif isinstance(comm, HostIpcGroup):
+                opts.comm_kind, opts.comm = GT_COMM_HOSTIPC, comm.handle
             else:
-                raise ValueError("world > 1 needs a LoopbackGroup or NcclComm")
+                raise ValueError("world > 1 needs a LoopbackGroup, NcclComm or HostIpcGroup")
         csr = _Csr(self.row_ptr.ctypes.data, self.col_idx.ctypes.data if nnz else None)
         h = _P()
         _check(L.gt_plan(ctypes.byref(csr), n, nnz, heads, d, world, ctypes.byref(opts), ctypes.byref(h)))

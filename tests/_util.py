@@ -38,6 +38,16 @@ def normwise(x, r):
     return num / den
 
 
+def elementwise(x, r, floor=1e-3):
+    """Reading Z8's diagnostic: max |x - r| / |r| over entries with |r| >= floor * max|r|."""
+    x = np.asarray(x, np.float64).ravel()
+    r = np.asarray(r, np.float64).ravel()
+    if r.size == 0 or np.max(np.abs(r)) == 0.0:
+        return 0.0
+    m = np.abs(r) >= floor * np.max(np.abs(r))
+    return float(np.max(np.abs(x[m] - r[m]) / np.abs(r[m])))
+
+
 TOL = {"f32": 1e-4, "bf16": 2e-2}
 LSE_TOL = {"f32": 1e-4, "bf16": 1e-2}
 

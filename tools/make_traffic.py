@@ -1,5 +1,11 @@
-"""Writes profiles/ncu_traffic.json: DRAM bytes (read + write) per launch of each profiled pass, from
-`ncu --set full` reports.  Usage: python tools/make_traffic.py <workload> stage=report.ncu-rep ..."""
+"""Records per-launch ncu counters of the profiled passes in profiles/ncu_traffic.json (read by bench.py
+for the physical roofline): DRAM bytes (read + write), L2 bytes (lts__t_bytes), executed warp
+instructions, issue / DRAM / L2 / L1 utilisation, and the sha256 of the kernel sources the report was
+taken from (bench.py flags the numbers as stale when the sources changed since).
+
+Usage: python tools/make_traffic.py [--out PATH] <workload> stage=report.ncu-rep|raw.csv ...
+"""
+import hashlib
 import json
 import os
 import sys
@@ -7,19 +13,66 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import summary  # noqa: E402
 
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "inst": 1, "%": 1}
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-data = json.load(open(path)) if os.path.exists(path) else {}
-wl = sys.argv[1]
-for arg in sys.argv[2:]:
-    stage, rep = arg.split("=", 1)
-    r = summary(rep)
-    tot = 0.0
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        v, u = r[k]
-        tot += float(v) * UNIT[u]
-    data.setdefault(wl, {})[stage] = tot
-    print(wl, stage, tot / 1e9, "GB")
-json.dump(data, open(path, "w"), indent=1)
+KERNEL_SOURCES = ("paper_2604_16715_b200/csrc/attn_pipe.cu",)   # the three pass kernels
+
+
+def kernel_sha(root=ROOT):
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        with open(os.path.join(root, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def val(r, k):
+    if k not in r:
+        return None
+    v, u = r[k]
+    try:
+        return float(v.replace(",", "")) * UNIT.get(u, 1)
+    except ValueError:
+        return None
+
+
+def ms(r):
+    v, u = r["gpu__time_duration.sum"]
+    return float(v.replace(",", "")) * {"msecond": 1.0, "ms": 1.0, "usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6,
+                                        "ns": 1e-6, "second": 1e3}.get(u, 1.0)
+
+
+def main(argv):
+    out = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if argv and argv[0] == "--out":
+        out, argv = argv[1], argv[2:]
+    data = json.load(open(out)) if os.path.exists(out) else {}
+    wl = argv[0]
+    for arg in argv[1:]:
+        stage, rep = arg.split("=", 1)
+        r = summary(rep)
+        rec = {
+            "dram_bytes": (val(r, "dram__bytes_read.sum") or 0) + (val(r, "dram__bytes_write.sum") or 0),
+            # bytes the SMs requested from L2 (L1TEX-sourced sectors x 32 B): the L2 -> SM roofline's numerator
+            "l2_bytes": (val(r, "lts__t_sectors_srcunit_tex.sum") or 0) * 32 or val(r, "lts__t_bytes.sum"),
+            "l2_fabric_bytes": (val(r, "lts__t_sectors_srcunit_ltcfabric.sum") or 0) * 32,
+            "inst": val(r, "smsp__inst_executed.sum"),
+            "ncu_ms": ms(r),
+            "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "dram_pct": val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l2_pct": val(r, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "l1_pct": val(r, "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+            "l2_hit_pct": val(r, "lts__t_sector_hit_rate.pct"),
+            "warps_active_pct": val(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "kernel": r["kernel"][:120],
+            "kernel_sha": kernel_sha(),
+            "report": os.path.basename(rep),
+        }
+        data.setdefault(wl, {})[stage] = rec
+        print(wl, stage, f"dram {rec['dram_bytes'] / 1e9:.2f} GB, l2 {(rec['l2_bytes'] or 0) / 1e9:.2f} GB, "
+                         f"issue {rec['issue_active_pct']} %")
+    json.dump(data, open(out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

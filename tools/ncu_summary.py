@@ -9,7 +9,8 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'launch__occupancy_limit_registers', 'launch__occupancy_limit_shared_mem', 'launch__grid_size',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'smsp__inst_executed.sum',
         'lts__throughput.avg.pct_of_peak_sustained_elapsed', 'l1tex__throughput.avg.pct_of_peak_sustained_active',
-        'lts__t_bytes.sum', 'sm__cycles_elapsed.avg.per_second']
+        'lts__t_bytes.sum', 'sm__cycles_elapsed.avg.per_second', 'lts__t_sectors_srcunit_tex.sum',
+        'lts__t_sectors_srcunit_ltcfabric.sum', 'lts__t_sectors.sum.pct_of_peak_sustained_elapsed']
 
 
 def summary(path):
