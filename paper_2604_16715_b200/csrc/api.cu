@@ -148,8 +148,9 @@ static void make_ag_pattern(const gt_plan_s* P, Pattern& pt) {
 static int64_t round16(int64_t x) { return (x + 15) / 16 * 16; }
 
 // Measured-beta profile (gt_opts.beta_profile; Fig. 2 / Alg. 3, reading Z14): a JSON object
-// {"allgather": B, "halo": B, "a2a": B} where B is seconds per exchanged row, either a number or an
-// object keyed by the GPU count ({"2": b2, "8": b8}, as written by paper_2604_16715_b200.agp).
+// {"allgather": B, "halo": B, "a2a": B, "row_bytes": R} where B is seconds per exchanged row of R bytes
+// (R absent: this plan's K||V row), either a number or an object keyed by the GPU count
+// ({"2": b2, "8": b8}, as written by paper_2604_16715_b200.agp --profile-out).
 // Returns NaN for a strategy the file does not give (that candidate is probed instead).
 static double profile_beta(const std::string& text, const char* name, int world) {
   const std::string key = std::string("\"") + name + "\"";
@@ -216,13 +217,22 @@ cudaEvent_t gt_plan_s::take_event() {
   cudaEventCreate(&e);
   return e;
 }
-void gt_plan_s::mark_begin(int, cudaStream_t st, cudaEvent_t* a) {
+// NVTX ranges (header-only NVTX3: no-ops unless a profiler injects itself) per stage, named like
+// gt_plan_timings' stages, plus one per entry point (NvtxScope).
+static const char* const kStageNames[5] = {"gt.fwd_exchange", "gt.fwd", "gt.bwd_rows", "gt.bwd_exchange",
+                                           "gt.bwd_cols"};
+void gt_plan_s::mark_begin(int stage, cudaStream_t st, cudaEvent_t* a) {
   *a = nullptr;
+  if (stage >= 0 && stage < 5) nvtx_id[stage] = nvtxRangeStartA(kStageNames[stage]);
   if (!profile) return;
   *a = take_event();
   cudaEventRecord(*a, st);
 }
 void gt_plan_s::mark_end(int stage, cudaStream_t st, cudaEvent_t a) {
+  if (stage >= 0 && stage < 5 && nvtx_id[stage]) {
+    nvtxRangeEnd(nvtx_id[stage]);
+    nvtx_id[stage] = 0;
+  }
   if (!profile || !a) return;
   cudaEvent_t b = take_event();
   cudaEventRecord(b, st);
@@ -607,7 +617,13 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       double t_ex = INFINITY;
       const double pb = prof.empty() ? NAN : profile_beta(prof, c == GT_ALLGATHER ? "allgather" : "halo", world);
       if (strategy == GT_AUTO && fits > 0 && std::isfinite(pb)) {
-        t_ex = pb * (double)(f.recv_rows + b.recv_rows);  // profiled beta x rows moved (Eq. 7 term)
+        // profiled beta x rows moved (Eq. 7 term).  A profile that states the row size it was measured at
+        // ("row_bytes", agp.py) is rescaled to this plan's rows (bandwidth regime: time ~ bytes); without
+        // it the profile is taken to be at this plan's K||V row size.
+        const double rb = prof.empty() ? NAN : profile_beta(prof, "row_bytes", world);
+        const double sf = (std::isfinite(rb) && rb > 0) ? (double)P->kv_row_bytes / rb : 1.0;
+        const double sb = (std::isfinite(rb) && rb > 0) ? (double)b_row / rb : 1.0;
+        t_ex = pb * ((double)f.recv_rows * sf + (double)b.recv_rows * sb);
       } else if (strategy == GT_AUTO && fits > 0) {
         // measure the forward and backward exchanges of this pattern (2 warm-up + 3 timed)
         DevBuf sb, rf, rb;
@@ -669,7 +685,8 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       if (misfit > 0 && strategy == GT_A2A) return fail(GT_ENOMEM, "gt_plan: GP-A2A buffers do not fit in device memory");
       const double pa = prof.empty() ? NAN : profile_beta(prof, "a2a", world);
       if (misfit == 0 && strategy == GT_AUTO && std::isfinite(pa)) {
-        const double t_ex = pa * 8.0 * (double)(n - P->n_local);
+        const double rb = profile_beta(prof, "row_bytes", world);  // head-group rows are gb bytes
+        const double t_ex = pa * 8.0 * (double)(n - P->n_local) * ((std::isfinite(rb) && rb > 0) ? (double)gb / rb : 1.0);
         P->info.beta_s_per_row[GT_A2A] = pa;
         P->info.predicted_ms[GT_A2A] = (t_iter1 / world + t_ex) * 1e3;
         P->info.agp_score[GT_A2A] = world * t_ex / (world - 1) * 1e3;
@@ -930,8 +947,14 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   return GT_OK;
 }
 
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+
 gt_status gt_plan(const gt_csr* csr, int64_t n, int64_t nnz, int heads, int d, int world, const gt_opts* opts,
                   gt_plan_t* out) {
+  NvtxScope nvtx("gt_plan");
   gt_opts def;
   if (!opts) {
     gt_default_opts(&def);
@@ -1306,6 +1329,7 @@ static gt_status graph_run(gt_plan_t P, std::vector<gt_plan_s::GraphEntry>& cach
 extern "C" {
 
 gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse, void* stream) {
+  NvtxScope nvtx("gt_attn_fwd");
   GT_TRY(check_ptrs(P, {q, k, v, y, lse}));
   cudaStream_t st = (cudaStream_t)stream;
   if (graph_ok(P, st, P->fwd_warm)) {
@@ -1322,6 +1346,7 @@ gt_status gt_attn_fwd(gt_plan_t P, const void* q, const void* k, const void* v, 
 
 gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, const void* y, const float* lse,
                       const void* dy, void* dq, void* dk, void* dv, void* stream) {
+  NvtxScope nvtx("gt_attn_bwd");
   GT_TRY(check_ptrs(P, {q, k, v, y, lse, dy, dq, dk, dv}));
   const bool fresh = logits_fresh(P, q, k, v, lse);
   cudaStream_t st = (cudaStream_t)stream;

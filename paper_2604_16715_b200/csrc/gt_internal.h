@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <array>
@@ -254,6 +255,7 @@ struct gt_plan_s {
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t take_event();
+  nvtxRangeId_t nvtx_id[5] = {0, 0, 0, 0, 0};   // open NVTX range per stage
   void mark_begin(int stage, cudaStream_t st, cudaEvent_t* a);
   void mark_end(int stage, cudaStream_t st, cudaEvent_t a);
   ~gt_plan_s();

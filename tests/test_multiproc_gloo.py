@@ -127,25 +127,43 @@ def _agp_worker(rank, world, port, result_q):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         from paper_2604_16715_b200 import agp
+        import paper_2604_16715_b200 as gt
 
-        beta, raw = agp.profile_beta(world, [2048, 8192, 32768], 256, torch.device("cpu"), reps=2)
+        import gtgen
+        rp, ci = gtgen.random_graph(3000, 40000, seed=17, directed=False, power=2.2, comm_size=512, f_in=0.9)
+        n = len(rp) - 1
+        beta, raw, per_row = agp.profile_beta(world, [2048, 8192, 32768], 256, torch.device("cpu"), reps=2,
+                                              graph=(rp, ci), N=n)
         if rank == 0:
-            for ci, c in enumerate(agp.COLLECTIVES):
+            for ci_, c in enumerate(agp.COLLECTIVES):
                 for p in range(2, world + 1):
-                    assert beta[ci, p] > 0 and np.isfinite(beta[ci, p]), (c, p)
-                    assert [r for r, _ in raw[c][p]] == [2048, 8192, 32768]
+                    assert beta[ci_, p] > 0 and np.isfinite(beta[ci_, p]), (c, p)
+                    assert per_row[c][p] > 0
+                    if c != "halo":
+                        assert [r for r, _ in raw[c][p]] == [2048, 8192, 32768]
+            # the halo candidate moves exactly the rows of libgt's send lists (forward + backward)
+            for p in range(2, world + 1):
+                b = gt.partition(rp, p)
+                want = sum(len(gt.send_list(rp, ci, b[s], b[s + 1], b[0], b[1], inward))
+                           for s in range(1, p) for inward in (False, True))
+                assert raw["halo"][p][0][0] == want
             # Alg. 3 on the profiled table: a huge t_iter(1) makes every candidate feasible (the argmin
             # is then the smallest score), a tiny one none (single GPU, reading Z12)
             big = agp.decide(1e6, 1e8, 1e6, beta)
             scores = {(c, p): v["score"] for c, d in big["estimates"].items() for p, v in d.items()}
             best = min(scores.values())
             assert big["score"] == best and big["strategy"] in agp.COLLECTIVES and big["gpus"] >= 2
+            assert set(big["estimates"]) == set(agp.COLLECTIVES)
             assert all(v["feasible"] for d in big["estimates"].values() for v in d.values())
             small = agp.decide(1e6, 1e8, 1e-12, beta)
             assert small["strategy"] == "single" and small["gpus"] == 1
             # Eq. 7 / 8 estimate = t1 / p + beta N
             est = big["estimates"]["allgather"][2]["t_iter_est_s"]
             assert abs(est - (1e6 / 2 + beta[0, 2] * 1e6)) <= 1e-9 * est
+            # halo wins Alg. 3 when its beta is the smallest
+            b2 = beta.copy()
+            b2[agp.COLLECTIVES.index("halo"), 2:] = 1e-15
+            assert agp.decide(1e6, 1e8, 1e6, b2)["strategy"] == "halo"
         dist.barrier()
         dist.destroy_process_group()
         result_q.put((rank, "ok"))
