@@ -44,6 +44,8 @@ def parse():
                     help="gt_opts.transport (world > 1): 0 copies, 1 fused peer gather over NVLink")
     ap.add_argument("--bwd-mode", type=int, default=0,
                     help="gt_opts.bwd_mode (world > 1): 0 transposed owner, 1 reduce-scatter of fp32 partials")
+    ap.add_argument("--kv-fp8", type=int, default=int(os.environ.get("GT_KV_FP8", "0")),
+                    help="gt_opts.kv_fp8: fp8 K||V storage (NEXT-4 option; not the bf16 headline)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -331,11 +333,14 @@ def sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs):
     y, lse = plan.fwd(tq, tk, tv)
     dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
     torch.cuda.synchronize()
-    out = {}
+    out, elem = {}, {}
     for name, got, ref in zip(("y", "dq", "dk", "dv"), (y, dq, dk, dv), refs):
         g = got.to(torch.float64).cpu().numpy()
         den = float(np.max(np.abs(ref))) or 1.0
         out[name] = float(np.max(np.abs(g - ref)) / den)
+        m = np.abs(ref) >= 1e-3 * den          # reading Z8's elementwise diagnostic (floor 1e-3 max|r|)
+        elem[name] = float(np.max(np.abs(g[m] - ref[m]) / np.abs(ref[m]))) if m.any() else 0.0
+    out["elementwise_diag"] = elem
     plan.close()
     out["tol"] = 2e-2 if cfg.dtype == "bf16" else 1e-4
     return out
@@ -423,7 +428,8 @@ def run_ours(args):
     t_plan = time.perf_counter()
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
                    strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local,
-                   edge_state=args.edge_state, bwd_mode=args.bwd_mode, transport=args.transport)
+                   edge_state=args.edge_state, bwd_mode=args.bwd_mode, transport=args.transport,
+                   kv_fp8=bool(args.kv_fp8))
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     info = plan.info()
@@ -540,7 +546,8 @@ def run_ours(args):
                              "no flush",
                        "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 512,
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
-                       "bwd_mode": info["bwd_mode"], "transport": info["transport"]},
+                       "bwd_mode": info["bwd_mode"], "transport": info["transport"],
+                       "kv_fp8": info["kv_fp8"]},
             "roofline": roofline,
             # whole step: ncu DRAM bytes of the three passes over the step time (physical), and the
             # no-reuse gather model (exceeds 1 on L2-local graphs: a model, not a fraction of the peak)

@@ -152,6 +152,17 @@ typedef struct {
                               once per set of tensor pointers, up to 4, and replayed).  Not used on
                               the legacy default stream or with profile = 1.  Small graphs, whose
                               steps are launch-bound, gain most. */
+  int kv_fp8;              /* 1 => fp8 K || V storage (reading Z25): gt_attn_fwd
+                              quantises k and v per (row, head) to e4m3 with a power-of-two scale 2^e
+                              (e the smallest integer with max |x| <= 448 2^e; x8 = RNE(x 2^-e)) into a
+                              plan-owned table [k8 | v8 | scales] (2 d h + 8 h B per row instead of
+                              4 d h), and the forward and the row pass gather it: the results are the
+                              attention of q, dY on the DEQUANTISED K^ = 2^e k8, V^ = 2^e v8 (products
+                              in f16 x e4m3 with fp32 accumulation; q and dY enter as f16 after a
+                              per-(row, head) power-of-two normalisation).  A backward whose k, v are
+                              not the last forward's re-quantises them.  Needs world == 1, a bf16
+                              plan, heads * d >= 128 and the materialised entry state (edge_state
+                              >= 0 and fitting); else GT_ECONFIG.  0 => K, V gathered as given. */
 } gt_opts;
 
 typedef struct {
@@ -181,6 +192,8 @@ typedef struct {
   int64_t fwd_gen;                /* gt_attn_fwd calls made on this plan */
   int64_t stale_bwds;             /* gt_attn_bwd calls whose (q, k, v, lse) were not those of the last
                                      gt_attn_fwd (they re-fetched / recomputed the forward's state) */
+  int kv_fp8;                     /* 1 if K, V are gathered from the plan's fp8 table (gt_opts.kv_fp8) */
+  int64_t kv_fp8_bytes;           /* device bytes of that table */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,
@@ -211,7 +224,11 @@ enum {
   GT_EXPORT_CSC_PTR = 5,    /* int64[n_local + 1] column pointers of the owned columns */
   GT_EXPORT_CSC_IDX = 6,    /* int32[nnz_in_local] global row ids, ascending within a column */
   GT_EXPORT_HEAVY_ROWS = 7, /* int32 local ids of rows split into chunks */
-  GT_EXPORT_HEAVY_COLS = 8  /* int32 local ids of columns split into chunks */
+  GT_EXPORT_HEAVY_COLS = 8, /* int32 local ids of columns split into chunks */
+  GT_EXPORT_KV8 = 9         /* uint8[n_local * row] the fp8 K || V table of the last quantisation
+                               (gt_opts.kv_fp8): per row k8[heads d] | v8[heads d] | 2^ek f32[heads] |
+                               2^ev f32[heads], padded to 16 B; len counts bytes.  Synchronises the
+                               device.  Empty when kv_fp8 is off. */
 };
 gt_status gt_plan_export(gt_plan_t plan, int what, int peer, void* dst, int64_t cap, int64_t* len);
 

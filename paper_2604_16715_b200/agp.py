@@ -273,7 +273,8 @@ def fig5_loopback(row_ptr, col_idx, heads: int, d: int, dtype: str, worlds, step
     t1 = sum(base.values()) * 1e-3
     rows = [{"p": 1, "strategy": "single", "measured_ms": t1 * 1e3, "stages_ms": base}]
     for p in worlds:
-        auto = run(p, "auto")[0][1]["strategy_name"]
+        auto_info = run(p, "auto")[0][1]        # GT_AUTO probes every candidate: its predictions
+        auto = auto_info["strategy_name"]
         for c in strategies:
             try:
                 res = run(p, c)
@@ -287,7 +288,8 @@ def fig5_loopback(row_ptr, col_idx, heads: int, d: int, dtype: str, worlds, step
             ci = {"allgather": 2, "halo": 3, "a2a": 4}[c]
             rows.append({"p": p, "strategy": c, "auto_choice": auto,
                          "eq7_estimate_ms": (t1 / p + beta * n) * 1e3,
-                         "plan_predicted_ms": info["predicted_ms"][ci] if np.isfinite(info["predicted_ms"][ci]) else None,
+                         "plan_predicted_ms": (auto_info["predicted_ms"][ci]
+                                               if np.isfinite(auto_info["predicted_ms"][ci]) else None),
                          "measured_ms": meas * 1e3, "measured_exchange_ms": exch * 1e3,
                          "beta_s_per_node": beta, "alg3_score_ms": p * beta * n / (p - 1) * 1e3,
                          "exch_bytes_rank0": info["exch_fwd_bytes"] + info["exch_bwd_bytes"]})

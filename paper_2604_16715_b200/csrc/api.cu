@@ -249,6 +249,8 @@ gt_plan_s::~gt_plan_s() {
   if (e2e_out) cudaStreamDestroy(e2e_out);
   for (cudaEvent_t e : e2e_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : e2e_cev)
+    if (e) cudaEventDestroy(e);
   if (ev_dq) cudaEventDestroy(ev_dq);
   for (auto* c : {&gfwd, &gbwd})
     for (auto& e : *c) cudaGraphExecDestroy(e.exec);
@@ -373,13 +375,17 @@ static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
   I.bwd_mode = P->bwd_reduce ? 1 : 0;
   I.transport = P->peer ? 1 : 0;
   if (P->peer) I.launches_fwd = launches_fwd(P) + 1;  // + the publish pack
+  I.kv_fp8 = P->kv_fp8 ? 1 : 0;
+  I.kv_fp8_bytes = P->kv_fp8 ? P->n_local * P->kv8_row : 0;
+  if (P->kv_fp8) I.launches_fwd += 1;                   // + the quantisation
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
                           &P->d_recv_kv, &P->d_recv_qd, &P->d_recv_st, &P->d_send_st, &P->d_s2, &P->d_pd, &P->d_src,
                           &P->d_hrow, &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx,
                           &P->d_hq, &P->d_hk, &P->d_hv, &P->d_hy, &P->d_hlse, &P->d_hdy, &P->d_hdq, &P->d_hdk,
-                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2], &P->d_pub, &P->d_iota, &P->d_pub_qd})
+                          &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2], &P->d_pub, &P->d_iota, &P->d_pub_qd,
+                          &P->d_kv8, &P->d_kvref})
     dev += (int64_t)b->bytes;
   if (P->strategy == GT_A2A && P->sub) {  // the world-1 plan over all rows with heads / world heads
     const gt_plan_info& S = P->sub->info;
@@ -488,6 +494,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   if (world > 1 && opts->transport == 1 && (world > 8 || opts->bwd_mode == 1))
     return fail(GT_ECONFIG, "gt_plan: the peer-gather transport needs world <= 8 and the transposed-owner backward");
   if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
+  if (opts->kv_fp8 != 0 && opts->kv_fp8 != 1) return fail(GT_EINVAL, "gt_plan: kv_fp8 must be 0 or 1");
+  if (opts->kv_fp8 && (world != 1 || opts->dtype != GT_BF16 || (int64_t)heads * d < 128 || opts->edge_state < 0))
+    return fail(GT_ECONFIG, "gt_plan: kv_fp8 needs world == 1, a bf16 plan, heads * d >= 128 and the entry state");
   if (opts->validate) GT_TRY(validate_csr(csr->row_ptr, csr->col_idx, n, nnz));
   else if (csr->row_ptr[n] != nnz) return fail(GT_EGRAPH, "row_ptr[n] != nnz");
 
@@ -924,6 +933,15 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
         for (auto* w : {&P->w_colp[0], &P->w_colp[1]}) GT_TRY(upload_work(*w));
       }
     }
+    // ---- fp8 K||V table (opts.kv_fp8) ----
+    if (opts->kv_fp8) {
+      if (!P->es) return fail(GT_ECONFIG, "gt_plan: kv_fp8 needs the entry state, which does not fit");
+      P->kv_fp8 = true;
+      P->kv8_row = (2 * D + 8 * heads + 15) / 16 * 16;
+      GT_TRY(P->d_kv8.alloc((size_t)std::max<int64_t>(P->n_local, 1) * P->kv8_row));
+      GT_CUDA_TRY(cudaMemset(P->d_kv8.p, 0, P->d_kv8.bytes));   // row padding stays zero
+      GT_TRY(P->d_kvref.alloc(2 * sizeof(int)));
+    }
     // ---- reduce-scatter backward (opts.bwd_mode = 1) ----
     if (P->bwd_reduce) GT_TRY(build_reduce_backward(P.get(), csr, rp_local, cols, full_row, c0, ag_of(P.get()),
                                                     P->strategy == GT_ALLGATHER ? pf_ag : pf_halo, T, st));
@@ -1026,6 +1044,17 @@ gt_status gt_plan_export(gt_plan_t P, int what, int peer, void* dst, int64_t cap
     }
     case GT_EXPORT_HEAVY_ROWS: src = P->heavy_rows.ids.data(); count = (int64_t)P->heavy_rows.ids.size(); break;
     case GT_EXPORT_HEAVY_COLS: src = P->heavy_cols.ids.data(); count = (int64_t)P->heavy_cols.ids.size(); break;
+    case GT_EXPORT_KV8: {
+      esz = 1;
+      count = P->kv_fp8 ? P->n_local * P->kv8_row : 0;
+      if (dst && count) {
+        if (cap < count) return fail(GT_EINVAL, "gt_plan_export: cap too small");
+        GT_CUDA_TRY(cudaDeviceSynchronize());
+        GT_CUDA_TRY(cudaMemcpy(dst, P->d_kv8.p, (size_t)count, cudaMemcpyDeviceToHost));
+      }
+      *len = count;
+      return GT_OK;
+    }
     default: return fail(GT_EINVAL, "gt_plan_export: unknown table");
   }
   *len = count;
@@ -1103,6 +1132,15 @@ static bool slices_fresh(gt_plan_t P, const void* q, const void* k, const void* 
   return P->slice_valid && P->slice_tag[0] == q && P->slice_tag[1] == k && P->slice_tag[2] == v;
 }
 
+// fp8 K||V table (gt_opts.kv_fp8) of these k, v
+static gt_status requantize(gt_plan_t P, const void* k, const void* v, cudaStream_t st) {
+  GT_TRY(quantize_kv(P->heads, P->heads * P->d, k, v, P->n_local, P->d_kv8.p, (int)P->kv8_row,
+                     P->d_kvref.as<int>(), st));
+  P->kv8_tag[0] = k;
+  P->kv8_tag[1] = v;
+  return GT_OK;
+}
+
 static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse,
                                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -1139,6 +1177,7 @@ static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const
     halo = P->d_recv_kv.p;
   }
   P->mark_begin(1, st, &ev);
+  if (P->kv_fp8) GT_TRY(requantize(P, k, v, st));
   GT_TRY(launch_fwd(P, q, k, v, halo, y, lse, st, P->world > 1 ? P->ev_halo : nullptr));
   P->mark_end(1, st, ev);
   set_fwd_tag(P, q, k, v, lse);
@@ -1204,6 +1243,10 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
       GT_TRY(fwd_exchange(P, k, v, st));
       GT_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_halo, 0));
     }
+  }
+  if (P->kv_fp8 && (P->kv8_tag[0] != k || P->kv8_tag[1] != v)) {  // the table holds another forward's k, v
+    GT_TRY(requantize(P, k, v, st));
+    stale = true;
   }
   if (stale) P->stale_bwds++;
   if (multi && P->bwd_reduce) {
@@ -1362,6 +1405,132 @@ gt_status gt_attn_bwd(gt_plan_t P, const void* q, const void* k, const void* v, 
   return GT_OK;
 }
 
+}  // extern "C"
+
+// Chunk bounds of a work list for the streamed host path: C contiguous ranges of about equal entry
+// counts, cut only at items of whole rows (columns) so a heavy row's chunks stay in one range;
+// t = item bounds, r = row (column) bounds, h = bounds in the heavy ids of `ct`.
+static void stream_bounds(const WorkList& w, const ChunkTable& ct, int64_t n_local, int C, std::vector<int64_t>& t,
+                          std::vector<int64_t>& r, std::vector<int64_t>& h) {
+  t.assign(1, 0);
+  r.assign(1, 0);
+  const int64_t E = w.n ? w.end[(size_t)w.n - 1] - w.beg[0] : 0;
+  int64_t x = 0;
+  for (int c = 1; c < C && w.n; ++c) {
+    const int64_t target = w.beg[0] + E * c / C;
+    x = std::max<int64_t>(x, t.back() + 1);
+    while (x < w.n && (w.beg[(size_t)x] < target || w.own[(size_t)x] < 0)) ++x;
+    if (x >= w.n) break;
+    t.push_back(x);
+    r.push_back(w.own[(size_t)x]);
+  }
+  t.push_back(w.n);
+  r.push_back(n_local);
+  h.clear();
+  for (int64_t b : r) h.push_back(std::lower_bound(ct.ids.begin(), ct.ids.end(), (int32_t)b) - ct.ids.begin());
+}
+
+// World-1 gt_attn_fwd_bwd_host, streamed in C row (column) chunks so that the host<->device copies
+// overlap the passes and each other (PCIe is full duplex): K, V go in first; then Q chunk c feeds
+// forward chunk c, whose Y / LSE rows leave at once; dY chunk c feeds row-pass chunk c, whose dQ rows
+// leave at once; the column pass (it needs every row's (P, dS)) runs in column chunks whose dK / dV
+// rows leave as they finish.  The arithmetic is that of gt_attn_fwd + gt_attn_bwd.
+static gt_status fwd_bwd_host_streamed(gt_plan_t P, const void* q, const void* k, const void* v, const void* dy,
+                                       void* y, float* lse, void* dq, void* dk, void* dv, cudaStream_t st) {
+  const int elt = P->dtype == GT_F32 ? 4 : 2;
+  const int64_t rb = (int64_t)P->heads * P->d * elt, lb = (int64_t)P->heads * 4;
+  if (!P->e2e_c) {
+    const char* env = std::getenv("GT_E2E_CHUNKS");
+    P->e2e_c = std::max(1, std::min(64, env ? std::atoi(env) : 8));
+    stream_bounds(P->w_rows, P->heavy_rows, P->n_local, P->e2e_c, P->e2e_t[0], P->e2e_r[0], P->e2e_h[0]);
+    stream_bounds(P->w_cols, P->heavy_cols, P->n_local, P->e2e_c, P->e2e_t[1], P->e2e_r[1], P->e2e_h[1]);
+    P->e2e_cev.assign(4 * (size_t)P->e2e_c + 4, nullptr);
+    for (auto& e : P->e2e_cev) GT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int Cr = (int)P->e2e_t[0].size() - 1, Cc = (int)P->e2e_t[1].size() - 1;
+  const auto& R = P->e2e_r[0];
+  const auto& Rc = P->e2e_r[1];
+  cudaEvent_t* ev = P->e2e_cev.data();            // [0, C) q in, [C, 2C) dy in, [2C, 3C) fwd, [3C, 4C) row pass
+  cudaEvent_t ev_start = P->e2e_ev[0], ev_kv = P->e2e_ev[1];
+  const int C = P->e2e_c;
+  char* dq_ = (char*)P->h2d[0].p;
+  char* dk_ = (char*)P->h2d[1].p;
+  char* dv_ = (char*)P->h2d[2].p;
+  char* ddy = (char*)P->h2d[3].p;
+  char* dy_ = (char*)P->h2d[4].p;
+  float* dl = P->h2d[5].as<float>();
+  char* ddq = (char*)P->h2d[6].p;
+  char* ddk = (char*)P->h2d[7].p;
+  char* ddv = (char*)P->h2d[8].p;
+  auto h2d = [&](char* dst, const void* src, int64_t r0, int64_t r1, int64_t row) -> gt_status {
+    if (r1 > r0)
+      GT_CUDA_TRY(cudaMemcpyAsync(dst + r0 * row, (const char*)src + r0 * row, (size_t)((r1 - r0) * row),
+                                  cudaMemcpyHostToDevice, P->e2e_in));
+    return GT_OK;
+  };
+  auto d2h = [&](void* dst, const char* src, int64_t r0, int64_t r1, int64_t row) -> gt_status {
+    if (dst && r1 > r0)
+      GT_CUDA_TRY(cudaMemcpyAsync((char*)dst + r0 * row, src + r0 * row, (size_t)((r1 - r0) * row),
+                                  cudaMemcpyDeviceToHost, P->e2e_out));
+    return GT_OK;
+  };
+  GT_CUDA_TRY(cudaEventRecord(ev_start, st));  // staging buffers are free once earlier work on `st` is done
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_in, ev_start, 0));
+  GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev_start, 0));
+  GT_TRY(h2d(dk_, k, 0, P->n_local, rb));
+  GT_TRY(h2d(dv_, v, 0, P->n_local, rb));
+  GT_CUDA_TRY(cudaEventRecord(ev_kv, P->e2e_in));
+  for (int c = 0; c < Cr; ++c) {
+    GT_TRY(h2d(dq_, q, R[c], R[c + 1], rb));
+    GT_CUDA_TRY(cudaEventRecord(ev[c], P->e2e_in));
+  }
+  for (int c = 0; c < Cr; ++c) {
+    GT_TRY(h2d(ddy, dy, R[c], R[c + 1], rb));
+    GT_CUDA_TRY(cudaEventRecord(ev[C + c], P->e2e_in));
+  }
+  // forward, in row chunks
+  GT_CUDA_TRY(cudaStreamWaitEvent(st, ev_kv, 0));
+  if (P->kv_fp8) GT_TRY(requantize(P, dk_, dv_, st));
+  for (int c = 0; c < Cr; ++c) {
+    GT_CUDA_TRY(cudaStreamWaitEvent(st, ev[c], 0));
+    GT_TRY(launch_pass_range(P, 0, dq_, dk_, dv_, nullptr, dl, nullptr, dy_, nullptr, st, P->e2e_t[0][c],
+                             P->e2e_t[0][c + 1], P->e2e_h[0][c], P->e2e_h[0][c + 1], c == 0));
+    GT_CUDA_TRY(cudaEventRecord(ev[2 * C + c], st));
+  }
+  set_fwd_tag(P, dq_, dk_, dv_, dl);
+  // row pass, in row chunks
+  for (int c = 0; c < Cr; ++c) {
+    GT_CUDA_TRY(cudaStreamWaitEvent(st, ev[C + c], 0));
+    GT_TRY(launch_pass_range(P, 1, dq_, dk_, dv_, dy_, dl, ddy, ddq, nullptr, st, P->e2e_t[0][c], P->e2e_t[0][c + 1],
+                             P->e2e_h[0][c], P->e2e_h[0][c + 1], c == 0));
+    GT_CUDA_TRY(cudaEventRecord(ev[3 * C + c], st));
+  }
+  // outputs of the forward and the row pass leave while the column pass runs
+  for (int c = 0; c < Cr; ++c) {
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev[2 * C + c], 0));
+    GT_TRY(d2h(y, dy_, R[c], R[c + 1], rb));
+    GT_TRY(d2h(lse, (const char*)dl, R[c], R[c + 1], lb));
+  }
+  for (int c = 0; c < Cr; ++c) {
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev[3 * C + c], 0));
+    GT_TRY(d2h(dq, ddq, R[c], R[c + 1], rb));
+  }
+  // column pass, in column chunks (reusing the forward's events, whose waits are already enqueued)
+  for (int c = 0; c < Cc; ++c) {
+    GT_TRY(launch_pass_range(P, 2, dq_, dk_, dv_, nullptr, nullptr, ddy, ddk, ddv, st, P->e2e_t[1][c],
+                             P->e2e_t[1][c + 1], P->e2e_h[1][c], P->e2e_h[1][c + 1], c == 0));
+    GT_CUDA_TRY(cudaEventRecord(ev[4 * C + (c & 3)], st));
+    GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev[4 * C + (c & 3)], 0));
+    GT_TRY(d2h(dk, ddk, Rc[c], Rc[c + 1], rb));
+    GT_TRY(d2h(dv, ddv, Rc[c], Rc[c + 1], rb));
+  }
+  GT_CUDA_TRY(cudaStreamSynchronize(P->e2e_out));
+  GT_CUDA_TRY(cudaStreamSynchronize(st));
+  return GT_OK;
+}
+
+extern "C" {
+
 gt_status gt_attn_fwd_bwd_host(gt_plan_t P, const void* q, const void* k, const void* v, const void* dy, void* y,
                                float* lse, void* dq, void* dk, void* dv, void* stream) {
   if (!P || !q || !k || !v || !dy) return fail(GT_EINVAL, "gt_attn_fwd_bwd_host: null input");
@@ -1384,6 +1553,9 @@ gt_status gt_attn_fwd_bwd_host(gt_plan_t P, const void* q, const void* k, const 
     for (cudaEvent_t* e : {&P->e2e_ev[0], &P->e2e_ev[1], &P->e2e_ev[2], &P->e2e_ev[3], &P->e2e_ev[4], &P->ev_dq})
       GT_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
+  const char* sm = std::getenv("GT_E2E_STREAM");  // A/B switch: "0" = the unchunked schedule below
+  if (P->world == 1 && !P->graphs && !(sm && sm[0] == '0'))
+    return fwd_bwd_host_streamed(P, q, k, v, dy, y, lse, dq, dk, dv, st);
   cudaEvent_t ev_start = P->e2e_ev[0], ev_qkv = P->e2e_ev[1], ev_dy = P->e2e_ev[2], ev_fwd = P->e2e_ev[3],
               ev_bwd = P->e2e_ev[4];
   GT_CUDA_TRY(cudaEventRecord(ev_start, st));  // staging buffers are free once earlier work on `stream` is

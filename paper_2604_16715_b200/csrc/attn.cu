@@ -307,6 +307,11 @@ int launches_bwd(const gt_plan_s* P) {
 static EntryState entry_state(gt_plan_s* P, int pass, bool use_logits = true) {
   EntryState e;
   if (!P->es) return e;
+  if (P->kv_fp8 && pass < 2) {  // fp8 K||V gathers (gt_opts.kv_fp8)
+    e.kv8 = P->d_kv8.p;
+    e.kv8_row = P->kv8_row;
+    e.kvref = P->d_kvref.as<int>();
+  }
   if (pass == 0) {
     if (P->es_logits) e.out = P->d_s2.as<float>();
   } else if (pass == 1) {
@@ -393,6 +398,47 @@ gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void
     m.y = (char*)y;
     m.lse = lse;
     GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 0, m, st));
+  }
+  return GT_OK;
+}
+
+// Streamed world-1 pass (gt_attn_fwd_bwd_host): work items [t0, t1) of the row (column) list - a
+// contiguous range of rows (columns) with every heavy row's chunks inside it - and the merges of the
+// heavy rows (columns) h0 .. h1 - 1 of the plan's chunk table among them.  fill: also the outputs of the
+// rows (columns) without entries.  pass 0: y, lse; 1: dq (+ the (LSE2, D) stats); 2: dk, dv.
+gt_status launch_pass_range(gt_plan_s* P, int pass, const void* q, const void* k, const void* v, const void* y,
+                            const float* lse, const void* dy, void* out_a, void* out_b, cudaStream_t st, int64_t t0,
+                            int64_t t1, int64_t h0, int64_t h1, bool fill) {
+  const ItemRange rg{t0, t1, fill};
+  const ChunkTable& ct = pass == 2 ? P->heavy_cols : P->heavy_rows;
+  const DevBuf& part = pass == 0 ? P->d_part_fwd : (pass == 1 ? P->d_part_rowb : P->d_part_colb);
+  if (pass == 0) {
+    GT_TRY(pipe_pass(P, 0, P->w_rows, ct, part.as<float>(), q, nullptr, nullptr, k, v, nullptr, nullptr, out_a,
+                     nullptr, const_cast<float*>(lse), st, 0, entry_state(P, 0), rg));
+  } else if (pass == 1) {
+    EntryState e = entry_state(P, 1, true);
+    e.own_c = y;
+    GT_TRY(pipe_pass(P, 1, P->w_rows, ct, part.as<float>(), q, dy, lse, k, v, nullptr, nullptr, out_a, nullptr,
+                     P->d_stats.as<float>(), st, 0, e, rg));
+  } else {
+    GT_TRY(pipe_pass(P, 2, P->w_cols, ct, part.as<float>(), k, v, nullptr, q, dy, nullptr, nullptr, out_a, out_b,
+                     nullptr, st, 0, entry_state(P, 2), rg));
+  }
+  if (h1 > h0) {
+    MergeArgs m = merge_args(ct, part, P->scale);
+    m.ids += h0;
+    m.first += h0;
+    m.nids = h1 - h0;
+    if (pass == 0) {
+      m.y = (char*)out_a;
+      m.lse = const_cast<float*>(lse);
+    } else if (pass == 1) {
+      m.dq = (char*)out_a;
+    } else {
+      m.dk = (char*)out_a;
+      m.dv = (char*)out_b;
+    }
+    GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, pass, m, st));
   }
   return GT_OK;
 }

@@ -155,6 +155,12 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
 
 template <typename T, int H, int D, int PASS, int ES>
 struct PC {
+  // ES bit 4: fp8 K||V gathers (gt_opts.kv_fp8; forward and row pass): the gathered table is the plan's
+  // quantised one, a row [k8 (D B) | v8 (D B) | 2^ek f32[H] | 2^ev f32[H]] (e4m3 with power-of-two
+  // scales per (row, head), quantize_kv_kernel)
+  static constexpr bool F8 = (ES & 4) != 0;
+  static constexpr int GR = F8 ? (2 * D + 8 * H + 15) / 16 * 16 : 0;   // bytes of a gathered fp8 row
+  static constexpr int LB8 = D / 32;                                    // bytes per lane of its fp8 slices
   static constexpr int RB = D * (int)sizeof(T);          // bytes of one feature row
   static constexpr int EPL = D / 32;                      // elements per lane
   static constexpr int LB = EPL * (int)sizeof(T);         // bytes per lane of one row (8..64)
@@ -164,17 +170,19 @@ struct PC {
   static constexpr int PDB = sizeof(T) == 2 ? 4 : 8;      // stored (P, dS) of one entry and head: bf16x2 | f32x2
   // the recompute column pass gathers each in-neighbour's (LSE2, D) block; with stored (P, dS) it does not
   static constexpr bool STATS = PASS == 2 && !(ES & 1);
-  static constexpr int EB = 2 * RB + (STATS ? SB : 0);                               // bytes per neighbour
+  static constexpr int EB = F8 ? GR : 2 * RB + (STATS ? SB : 0);                     // bytes per neighbour
   // own slot: fwd q | rowb [q] dY Y lse | colb [k v]   (the row pass recomputing q.k needs q; with
   // stored (P, dS) the column pass needs no own-column data)
   static constexpr int OWN_DY = PASS == 1 ? ((ES & 2) ? 0 : RB) : 0;
   static constexpr int OWN_Y = OWN_DY + RB;
-  static constexpr int OWN_LSE = OWN_Y + RB;
-  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * H : ((ES & 1) ? 0 : 2 * RB));
+  static constexpr int OWN_LSE = OWN_Y + RB;   // the row's LSE of the lane's head, one 4-byte slot per lane
+  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * 32 : ((ES & 1) ? 0 : 2 * RB));
 #ifdef GT_PIPE_U  // tuning override (A/B builds)
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : (GT_PIPE_U * H <= 32 ? GT_PIPE_U : 32 / H));
 #else
-  static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4);                  // neighbours per stage
+  // neighbours per stage (fp8: 4; 8 in two butterfly groups measured slower on C3 / C5: fwd 10.7 -> 11.1 /
+  // 31.7 -> 40.3 ms)
+  static constexpr int U = F8 ? 4 : (RB >= 2048 ? 1 : (RB >= 1024 ? 2 : 4));
 #endif
   // per-stage entry state gathered into the stage (ES): rowb s2[U][H] f32 (the forward's logits),
   // colb (P, dS)[U][H] (the row pass's)
@@ -182,7 +190,7 @@ struct PC {
   // TMA gathers (sm_100 cp.async.bulk.tensor tile::gather4: 4 rows of a 2-D tensor map per instruction)
   // for the two feature rows of every neighbour when the stage holds exactly 4 neighbours; the
   // stage then keeps the 4 first rows (k | q) contiguous, then the 4 second rows (v | dY), then stats
-  static constexpr bool TMA = GT_PIPE_TMA && U == 4;
+  static constexpr bool TMA = GT_PIPE_TMA && U == 4 && !F8;
   static constexpr int STAGE = (U * EB + AUX + 127) / 128 * 128;   // 128-byte aligned TMA destinations
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
   // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dS)[U][H]
@@ -192,10 +200,13 @@ struct PC {
   // byte offsets in a stage of neighbour u's first row, second row and (LSE2, D) block (tma: the kernel
   // gathers with TMA; kernels with remote rows keep the interleaved per-lane-copy layout)
   template <bool TM> static __device__ __forceinline__ int koff(int u) { return TM ? u * RB : u * EB; }
-  template <bool TM> static __device__ __forceinline__ int voff(int u) { return TM ? U * RB + u * RB : u * EB + RB; }
+  template <bool TM> static __device__ __forceinline__ int voff(int u) {
+    return TM ? U * RB + u * RB : u * EB + (F8 ? D : RB);
+  }
   template <bool TM> static __device__ __forceinline__ int soff(int u) { return TM ? 2 * U * RB + u * SB : u * EB + 2 * RB; }
   static_assert(LB == 4 || LB == 8 || LB % 16 == 0, "lane slice must be 4, 8 or a multiple of 16 bytes");
   static_assert(U * H <= 32, "entry-state copies: one lane per (neighbour, head)");
+  static_assert(!F8 || (sizeof(T) == 2 && PASS < 2 && LB8 >= 4 && 32 / H >= 4), "fp8 gathers: bf16 plans, D >= 128");
 };
 
 struct PArgs {
@@ -233,6 +244,7 @@ struct PArgs {
                          // bf16 plans, f32x2 for f32 plans), both in local CSR entry order
   const float* es_in;    // rowb: s2 | colb: (P, dS)
   const int32_t* src;    // colb: local CSC position -> local CSR entry (read through a window like nbr)
+  const int* kvref;      // fp8 gathers: {E_k, E_v} = max exponent of the K / V scales over the table
   uint32_t rb, rb2, sb;  // row strides (bytes) of the gathered tables as run-time values: a row address is
                          // then one IMAD.WIDE.U32 (an immediate power-of-two stride becomes shift + high +
                          // two 64-bit adds)
@@ -450,6 +462,104 @@ __device__ __forceinline__ void accum(uint32_t wb, const uint32_t (&x)[W], float
   }
 }
 
+// ---- fp8 (e4m3) gathers: decoded to f16 and multiplied by f16 operands with fp32 accumulation ----
+__device__ __forceinline__ float fma_f16(uint16_t a, uint16_t b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t f16x2_of(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint16_t f16_of(float x) {   // saturating: |x| > 65504 -> +-65504
+  uint16_t r;
+  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t x16) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"((uint16_t)x16));
+  return r;
+}
+// 2^e for e in [-126, 127] (exact)
+__device__ __forceinline__ float exp2i(int e) { return __int_as_float((e + 127) << 23); }
+// floor(log2 |x|) of a positive normal float, clamped to [-126, 126] (x == 0: 0)
+__device__ __forceinline__ int ilog2f(float x) {
+  const int e = ((__float_as_int(x) >> 23) & 0xff) - 127;
+  return x > 0.f ? max(-126, min(126, e)) : 0;
+}
+// the lane's EPL fp8 elements (EPL / 4 words) from shared memory
+template <int EPL>
+__device__ __forceinline__ void lds_f8(const char* p, uint32_t (&w)[EPL / 4]) {
+  constexpr int NW = EPL / 4;
+  if constexpr (NW == 4) {
+    const uint4 x = *reinterpret_cast<const uint4*>(p);
+    w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+  } else if constexpr (NW == 2) {
+    const uint2 x = *reinterpret_cast<const uint2*>(p);
+    w[0] = x.x; w[1] = x.y;
+  } else {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  }
+}
+// <o, x> with o the lane's EPL elements as f16x2 words and x its EPL fp8 elements
+template <int EPL>
+__device__ __forceinline__ float dot_f8(const uint32_t (&o)[EPL / 2], const uint32_t (&x)[EPL / 4]) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < EPL / 4; ++i) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const uint32_t f = e4m3x2_to_f16x2(hh ? x[i] >> 16 : x[i] & 0xffffu);  // elements 4i + 2hh, +1
+      uint16_t fl, fh, ol, oh;
+      asm("mov.b32 {%0, %1}, %2;" : "=h"(fl), "=h"(fh) : "r"(f));
+      asm("mov.b32 {%0, %1}, %2;" : "=h"(ol), "=h"(oh) : "r"(o[2 * i + hh]));
+      s0 = fma_f16(ol, fl, s0);
+      s1 = fma_f16(oh, fh, s1);
+    }
+  }
+  return s0 + s1;
+}
+// acc += w x over the lane's EPL fp8 elements, w an f16
+template <int EPL>
+__device__ __forceinline__ void accum_f8(uint16_t w, const uint32_t (&x)[EPL / 4], float (&acc)[EPL]) {
+#pragma unroll
+  for (int i = 0; i < EPL / 4; ++i) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const uint32_t f = e4m3x2_to_f16x2(hh ? x[i] >> 16 : x[i] & 0xffffu);
+      uint16_t fl, fh;
+      asm("mov.b32 {%0, %1}, %2;" : "=h"(fl), "=h"(fh) : "r"(f));
+      acc[4 * i + 2 * hh] = fma_f16(w, fl, acc[4 * i + 2 * hh]);
+      acc[4 * i + 2 * hh + 1] = fma_f16(w, fh, acc[4 * i + 2 * hh + 1]);
+    }
+  }
+}
+
+// The lane's EPL bf16 elements (raw words) scaled by 2^-e, e = floor(log2 max |x|) over the lane's head
+// (the largest is then in [1, 2): exact in f16 unless 2^14 times smaller than the max), as f16x2 words.
+template <int EPL, int LPH>
+__device__ __forceinline__ int to_f16_norm(const uint32_t (&w)[EPL / 2], uint32_t (&o)[EPL / 2]) {
+  float f[EPL];
+#pragma unroll
+  for (int i = 0; i < EPL / 2; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+  float am = 0.f;
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) am = fmaxf(am, fabsf(f[i]));
+#pragma unroll
+  for (int o2 = LPH / 2; o2 >= 1; o2 >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o2));
+  const int e = ilog2f(am);
+  const float sc = exp2i(-e);
+#pragma unroll
+  for (int i = 0; i < EPL / 2; ++i) o[i] = f16x2_of(f[2 * i] * sc, f[2 * i + 1] * sc);
+  return e;
+}
+
 // predicated 32-bit global store of raw bits
 __device__ __forceinline__ void st_pred_u32(uint32_t* p, uint32_t x, bool on) {
   asm volatile("{.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;}" ::"l"(p), "r"(x),
@@ -520,7 +630,9 @@ struct Meta {      // warp-uniform description of one filled stage
 #define GT_CARVEOUT -1
 #endif
 template <int PASS, int ES, int EPL>
-constexpr int min_ctas() { return EPL > 8 ? 1 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : GT_FWD_MINB)); }
+constexpr int min_ctas() {
+  return EPL > 8 ? 1 : ((ES & 4) ? 5 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : GT_FWD_MINB)));
+}
 
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
 __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
@@ -571,6 +683,8 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
   int32_t wsrc = 0, wsrc_next = 0;   // ES column pass: src[] over the same window
   // this lane's slice of row 0 of every gathered table: a row address is one mad.wide.u32
   const char* const ga_l = a.ga + lane * LB;
+  const char* const g8_l = C::F8 ? a.ga + lane * C::LB8 : nullptr;       // fp8: the lane's k8 slice
+  const char* const gs8_l = C::F8 ? a.ga + 2 * D + lane * 16 : nullptr;  // fp8: 16 B of the scales
   const char* const gb_l = a.gb + lane * LB;
   const char* const h_l = HALO ? a.halo + lane * LB : nullptr;
   const char* const gs_l = PASS == 2 ? a.gs + lane * 16 : nullptr;
@@ -694,6 +808,18 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
             cp_async16z(st + C::template soff<kTma>(u) + lane * 16, row_addr(gs_l, (uint32_t)(u < cnt ? id[u] : id[0]), C::SB),
                         u < cnt);
       }
+    } else if constexpr (C::F8) {
+      // fp8 K||V rows: the lane's k8 and v8 slices off one row address, the scales by the first lanes
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool valid = u < cnt;
+        const uint32_t cv = (uint32_t)__shfl_sync(kFull, win, off + u);
+        const char* pr = row_addr(g8_l, cv, sRB);
+        char* dst = st + u * EB + lane * C::LB8;
+        cp_lane_z<C::LB8>(dst, pr, valid);
+        cp_lane_z<C::LB8>(dst + D, pr + D, valid);
+        if (lane < (8 * H + 15) / 16) cp_async16z(st + u * EB + 2 * D + lane * 16, row_addr(gs8_l, cv, sRB), valid);
+      }
     } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // branch-free: neighbours u >= cnt are zero-filled, not read
@@ -761,7 +887,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         if constexpr (!(ES & 2)) cp_slice<LB>(o, a.oa + r * RB, lane);
         cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
         cp_slice<LB>(o + C::OWN_Y, a.oc + r * RB, lane);
-        cp_async<4>(o + C::OWN_LSE + head * 4, a.lse + r * H + head);
+        cp_async<4>(o + C::OWN_LSE + lane * 4, a.lse + r * H + head);  // distinct slots: no same-address writes
       } else if constexpr (!(ES & 1)) {
         cp_slice<LB>(o, a.oa + r * a.own_stride, lane);
         cp_slice<LB>(o + RB, a.ob + r * a.own_stride, lane);
@@ -778,6 +904,12 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
   uint32_t ow[W];             // raw own-row words: q (fwd), dY (rowb), k (colb recompute)
   uint32_t ow2[W];            // rowb recompute: q; colb recompute: v
   float m = 0.f, l = 0.f;     // fwd: running max / sum (base 2) | rowb: lse2 (m), D (l)
+  // fp8 gathers: own row as normalised f16 (fwd q', rowb dY' and, without stored logits, q') and its
+  // factors (fwd: qscale 2^eq; rowb: 2^e_dy, qscale 2^eq); table references 2^E_k, 2^E_v
+  uint32_t oh[C::F8 ? EPL / 2 : 1], oq[(C::F8 && PASS == 1 && !(ES & 2)) ? EPL / 2 : 1];
+  float fo = 1.f, ifo = 1.f, fq = 1.f;
+  const float rk = C::F8 ? exp2i(__ldg(a.kvref)) : 1.f, rv = C::F8 ? exp2i(__ldg(a.kvref + 1)) : 1.f;
+  const float irk = 1.f / rk, irv = 1.f / rv;
 
   Meta md[kS];
 #pragma unroll
@@ -789,7 +921,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
       cp_wait<kS - 1>();
-      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2))) __syncwarp();  // blocks copied by other lanes
+      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8) __syncwarp();  // blocks copied by other lanes
       const Meta cur = md[s];
       if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one (no copy in flight)
       if constexpr (kTma) {
@@ -801,6 +933,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         const char* o = owns + s * C::OWNP;
         if constexpr (PASS == 0) {
           lds_raw<W>(o + lane * LB, ow);
+          if constexpr (C::F8) fo = a.qscale * exp2i(to_f16_norm<EPL, LPH>(ow, oh));
 #pragma unroll
           for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
           m = -INFINITY;
@@ -812,7 +945,13 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
           lds_raw<W>(o + C::OWN_Y + lane * LB, yw);
           // D_i = sum_e P_e dP_e = <dY_i, sum_e P_e v_j> = <dY_i, Y_i> (Sum_e P_e = 1)
           l = head_sum<LPH>(dot_raw<T, W>(ow, yw));
-          m = reinterpret_cast<const float*>(o + C::OWN_LSE)[head] * kLog2e;
+          m = reinterpret_cast<const float*>(o + C::OWN_LSE)[lane] * kLog2e;
+          if constexpr (C::F8) {
+            const int e = to_f16_norm<EPL, LPH>(ow, oh);
+            fo = exp2i(e);
+            ifo = exp2i(-e);
+            if constexpr (!(ES & 2)) fq = a.qscale * exp2i(to_f16_norm<EPL, LPH>(ow2, oq));
+          }
 #pragma unroll
           for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
         } else {
@@ -825,7 +964,105 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         }
       }
       const int cnt = cur.cnt;
-      if constexpr (PASS == 0 && kBfly) {
+      if constexpr (C::F8 && PASS == 0) {
+        // fp8 forward: s = qscale 2^eq 2^ek_j <q', k8_j>, p~ = 2^(s - m), acc += f16(p~ 2^(ev_j - E_v)) v8_j
+        // (y = acc 2^E_v / l); the dots are reduce-scattered by the butterfly as in the bf16 path, in
+        // groups of 4 neighbours
+        using B = Bfly<LPH>;
+#pragma unroll
+        for (int g0 = 0; g0 < U; g0 += 4) {
+        float part[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t kx[EPL / 4];
+          lds_f8<EPL>(st + C::template koff<false>(g0 + u) + lane * C::LB8, kx);
+          part[u] = dot_f8<EPL>(oh, kx);
+        }
+        const float r = B::reduce(part, lane);
+        const int ug = g0 + B::group(lane);
+        const float* scl = reinterpret_cast<const float*>(st + ug * EB + 2 * D);
+        const float sv = r * fo * scl[head];
+        const float sl = ug < cnt ? sv : -INFINITY;
+        if constexpr (ES & 2) reinterpret_cast<float*>(xs + s * C::XS)[ug * H + head] = sv;
+        const float mx = fmaxf(B::all_max(sl), m);
+        const float corr = ex2(m - mx);
+        l *= corr;
+        scale2<EPL>(corr, acc);
+        const float pl = ex2(sl - mx);
+        l += pl;
+        const uint32_t wl = f16_of(pl * scl[H + head] * irv);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
+          uint32_t vx[EPL / 4];
+          lds_f8<EPL>(st + C::template voff<false>(g0 + u) + lane * C::LB8, vx);
+          accum_f8<EPL>((uint16_t)w, vx, acc);
+        }
+        m = mx;
+        }
+        if constexpr (ES & 2) {  // s2 of the stage's entries: one coalesced store
+          __syncwarp();
+          const float* x = reinterpret_cast<const float*>(xs + s * C::XS);
+          st_pred(a.es_out + (int64_t)cur.e0 * H + lane, x[lane < U * H ? lane : 0], lane < cnt * H);
+        }
+      } else if constexpr (C::F8 && PASS == 1) {
+        // fp8 row pass: dP = 2^e_dy 2^ev_j <dY', v8_j>, p = 2^(s - lse2), dS = p (dP - D),
+        // acc += f16(dS 2^-e_dy 2^(ek_j - E_k)) k8_j   (dQ = scale 2^e_dy 2^E_k acc)
+        using B = Bfly<LPH>;
+#pragma unroll
+        for (int g0 = 0; g0 < U; g0 += 4) {
+        float part[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t vx[EPL / 4];
+          lds_f8<EPL>(st + C::template voff<false>(g0 + u) + lane * C::LB8, vx);
+          part[u] = dot_f8<EPL>(oh, vx);
+        }
+        const float dr = B::reduce(part, lane);
+        const int ug = g0 + B::group(lane);
+        const float* scl = reinterpret_cast<const float*>(st + ug * EB + 2 * D);
+        const float dpl = dr * fo * scl[H + head];
+        float s_;
+        if constexpr (ES & 2) {
+          s_ = reinterpret_cast<const float*>(st + U * EB)[ug * H + head];  // forward's logit
+        } else {
+          float pq[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t kx[EPL / 4];
+            lds_f8<EPL>(st + C::template koff<false>(g0 + u) + lane * C::LB8, kx);
+            pq[u] = dot_f8<EPL>(oq, kx);
+          }
+          s_ = B::reduce(pq, lane) * fq * scl[head];
+        }
+        const float pl = ug < cnt ? ex2(s_ - m) : 0.f;
+        const float dsl = pl * (dpl - l);
+        if constexpr (ES & 1) {
+          if constexpr (C::PDB == 4) reinterpret_cast<uint32_t*>(xs + s * C::XS)[ug * H + head] = pack_pd_bf16(pl, dsl);
+          else reinterpret_cast<float2*>(xs + s * C::XS)[ug * H + head] = make_float2(pl, dsl);
+        }
+        const uint32_t wl = f16_of(dsl * ifo * scl[head] * irk);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w = __shfl_sync(kFull, wl, B::src(lane, u));
+          uint32_t kx[EPL / 4];
+          lds_f8<EPL>(st + C::template koff<false>(g0 + u) + lane * C::LB8, kx);
+          accum_f8<EPL>((uint16_t)w, kx, acc);
+        }
+        }
+        if constexpr (ES & 1) {
+          constexpr int NW = U * H * C::PDB / 4;
+          constexpr int EW = H * C::PDB / 4;
+          __syncwarp();
+          const uint32_t* x = reinterpret_cast<const uint32_t*>(xs + s * C::XS);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(a.es_out) + (int64_t)cur.e0 * EW;
+#pragma unroll
+          for (int t = 0; t < (NW + 31) / 32; ++t) {
+            const int f = lane + 32 * t;
+            st_pred_u32(dst + f, x[f < NW ? f : 0], f < cnt * EW);
+          }
+        }
+      } else if constexpr (PASS == 0 && kBfly) {
         // Transposed (reduce-scatter) butterfly over the head's lanes (Bfly): the 4 per-lane partial dot
         // products of the stage are summed so that each lane group ends up with one neighbour's full
         // score (14 instructions instead of 4 x 6 at 8 lanes per head); max and exp are then taken once
@@ -1009,12 +1246,12 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
           if constexpr (PASS == 0) {
             float* pp = a.part + ch * (int64_t)(D + 2 * H);
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
+            for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = C::F8 ? acc[i] * rv : acc[i];
             { pp[D + 2 * head] = m; pp[D + 2 * head + 1] = l; }
           } else if constexpr (PASS == 1) {
             float* pp = a.part + ch * (int64_t)D;
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = acc[i];
+            for (int i = 0; i < EPL; ++i) pp[lane * EPL + i] = C::F8 ? acc[i] * (fo * rk) : acc[i];
           } else {
             float* pp = a.part + ch * (int64_t)(2 * D);
 #pragma unroll
@@ -1023,14 +1260,15 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         } else {
           if constexpr (PASS == 0 && kBfly) l = Bfly<LPH>::all_sum(l);
           if constexpr (PASS == 0) {
-            const float inv = 1.f / l;
+            const float inv = (C::F8 ? rv : 1.f) / l;
 #pragma unroll
             for (int i = 0; i < EPL; ++i) acc[i] *= inv;
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
             a.out_f[r * H + head] = (m + __log2f(l)) * kLn2;
           } else if constexpr (PASS == 1) {
+            const float f = C::F8 ? a.scale * fo * rk : a.scale;
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) acc[i] *= a.scale;
+            for (int i = 0; i < EPL; ++i) acc[i] *= f;
             stg_f32<T, EPL>(a.out_a + r * RB + lane * LB, acc);
           } else {
 #pragma unroll
@@ -1040,7 +1278,10 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
           }
         }
       }
-      md[s] = produce(s);   // refill the stage just consumed (this lane's own slices only)
+      // stage blocks other lanes read (entry state, stats) are refilled by the lanes that copy them:
+      // order those reads before the new copies (formally, under independent thread scheduling)
+      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8) __syncwarp();
+      md[s] = produce(s);   // refill the stage just consumed
       cp_commit();
     }
   }
@@ -1077,6 +1318,86 @@ gt_status fill_empty(int pass, const int32_t* ids, int64_t n, char* out_a, char*
   else fill_empty_kernel<2><<<blocks, 256, 0, st>>>(ids, n, out_a, out_b, out_f, rb, heads, sb);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
+}
+
+// ------------------------------------------------------------ fp8 K||V table --
+// gt_opts.kv_fp8 (NEXT-4): K and V quantised per (row, head) to e4m3 with a power-of-two scale 2^e,
+// e the smallest integer with max |x| <= 448 2^e (448 = e4m3's largest finite value), x8 = RNE(x 2^-e)
+// (exact scaling, one rounding; reading Z25).  Row layout [k8 | v8 | 2^ek f32[H] | 2^ev f32[H]], padded
+// to 16 B; ref = {max ek, max ev} over the table (the kernels' f16 weights are taken relative to it).
+template <int H, int D>
+__global__ void __launch_bounds__(256) quantize_kv_kernel(const uint32_t* k, const uint32_t* v, int64_t n, char* out,
+                                                          int gr, int* ref) {
+  constexpr int EPL = D / 32, LPH = 32 / H, W = EPL / 2;
+  const int lane = threadIdx.x & 31, head = lane / LPH;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int emax[2] = {-126, -126};
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t* src = (t ? v : k) + r * (D / 2) + lane * W;
+      float f[EPL];
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        const uint32_t x = __ldg(src + i);
+        f[2 * i] = __uint_as_float(x << 16);
+        f[2 * i + 1] = __uint_as_float(x & 0xffff0000u);
+      }
+      float am = 0.f;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) am = fmaxf(am, fabsf(f[i]));
+#pragma unroll
+      for (int o = LPH / 2; o >= 1; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+      int e = -126;
+      if (am > 0.f) {
+        const int bits = __float_as_int(am);
+        const int E = ((bits >> 23) & 0xff) - 127;
+        e = (bits & 0x7fffff) <= 0x600000 ? E - 8 : E - 7;   // 1.m 2^E <= 1.75 2^(8 + e), e minimal
+        e = max(-126, min(126, e));
+      }
+      emax[t] = max(emax[t], e);
+      const float sc = __int_as_float((127 - e) << 23);    // 2^-e
+      uint32_t w8[EPL / 4];
+#pragma unroll
+      for (int i = 0; i < EPL / 2; ++i) {
+        uint16_t b;
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(b) : "f"(f[2 * i + 1] * sc), "f"(f[2 * i] * sc));
+        if (i % 2 == 0) w8[i / 2] = b;
+        else w8[i / 2] |= (uint32_t)b << 16;
+      }
+      char* dst = out + r * gr + t * D + lane * (EPL);
+      if constexpr (EPL / 4 == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+      else if constexpr (EPL / 4 == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(w8[0], w8[1]);
+      else *reinterpret_cast<uint32_t*>(dst) = w8[0];
+      if (lane % LPH == 0)
+        reinterpret_cast<float*>(out + r * gr + 2 * D)[t * H + head] = __int_as_float((e + 127) << 23);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    int x = emax[t];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) atomicMax(ref + t, x);
+  }
+}
+
+gt_status quantize_kv_impl(int H, int D, const void* k, const void* v, int64_t n, void* out, int gr, int* ref,
+                           cudaStream_t st) {
+  GT_CUDA_TRY(cudaMemsetAsync(ref, 0x80, 2 * sizeof(int), st));  // INT_MIN-like start for the max
+  if (n <= 0) return GT_OK;
+  const int blocks = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 16);
+#define GT_Q(HH, DD)                                                                                         \
+  if (H == HH && D == DD) {                                                                                  \
+    quantize_kv_kernel<HH, DD><<<blocks, 256, 0, st>>>((const uint32_t*)k, (const uint32_t*)v, n, (char*)out, gr, \
+                                                       ref);                                                 \
+    GT_CUDA_TRY(cudaGetLastError());                                                                         \
+    return GT_OK;                                                                                            \
+  }
+  GT_Q(1, 128) GT_Q(2, 128) GT_Q(4, 128) GT_Q(8, 128) GT_Q(1, 256) GT_Q(2, 256) GT_Q(4, 256) GT_Q(8, 256)
+  GT_Q(1, 512) GT_Q(2, 512) GT_Q(4, 512) GT_Q(8, 512)
+#undef GT_Q
+  return fail(GT_ECONFIG, "kv_fp8: unsupported (heads, heads * d)");
 }
 
 // ----------------------------------------------------------------- launcher --
@@ -1156,6 +1477,14 @@ struct Ops {
   // ES bits: 1 = (P, dP) materialised (rowb stores, colb reads), 2 = logits materialised (fwd stores,
   // rowb reads)
   static gt_status run(int pass, const PArgs& a, cudaStream_t st, int rs) {
+    if (a.kvref) {  // fp8 K||V gathers (world 1, bf16, heads * d >= 128)
+      if constexpr (sizeof(T) == 2 && D >= 128) {
+        if (pass == 0) return a.es_out ? launch<T, H, D, 0, false, 6>(a, st, rs) : launch<T, H, D, 0, false, 4>(a, st, rs);
+        if (pass == 1 && a.es_out)
+          return a.es_in ? launch<T, H, D, 1, false, 7>(a, st, rs) : launch<T, H, D, 1, false, 5>(a, st, rs);
+      }
+      return fail(GT_ECONFIG, "kv_fp8: unsupported pass / shape");
+    }
     if (pass == 0) {
       if (a.halo) return a.es_out ? launch<T, H, D, 0, true, 2>(a, st, rs) : launch<T, H, D, 0, true, 0>(a, st, rs);
       return a.es_out ? launch<T, H, D, 0, false, 2>(a, st, rs) : launch<T, H, D, 0, false, 0>(a, st, rs);
@@ -1199,18 +1528,24 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
 
 }  // namespace pipe
 
+gt_status quantize_kv(int H, int D, const void* k, const void* v, int64_t n, void* out, int gr, int* ref,
+                      cudaStream_t st) {
+  return pipe::quantize_kv_impl(H, D, k, v, n, out, gr, ref, st);
+}
+
 // Runs one pass of the pipelined kernel over the work list `w` (chunks of `ct` write partial states
 // to `part`; their merges are launched by the caller).
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
                     const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
                     const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms,
-                    const EntryState& es) {
+                    const EntryState& es, const ItemRange& range) {
   pipe::PArgs a{};
   const bool rows = pass != 2;
-  a.ibeg = w.d_beg.as<int64_t>();
-  a.iend = w.d_end.as<int64_t>();
-  a.iown = w.d_own.as<int32_t>();
-  a.nitems = w.n;
+  const int64_t t0 = std::min<int64_t>(range.t0, w.n), t1 = range.t1 < 0 ? w.n : std::min<int64_t>(range.t1, w.n);
+  a.ibeg = w.d_beg.as<int64_t>() + t0;
+  a.iend = w.d_end.as<int64_t>() + t0;
+  a.iown = w.d_own.as<int32_t>() + t0;
+  a.nitems = std::max<int64_t>(t1 - t0, 0);
   a.cown = ct.d_owner.as<int32_t>();
   a.nbr = es.nbr ? es.nbr : (rows ? P->d_col : P->d_row).as<int32_t>();
   a.nnbr = es.nbr ? es.nnbr : (rows ? P->nnz_local : P->nnz_in_local);
@@ -1244,7 +1579,13 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.es_out = es.out;
   a.es_in = es.in;
   a.src = es.src;
-  if (!w.empty.empty())
+  if (es.kv8 && pass < 2) {  // fp8 K||V table replaces the two gathered tables
+    a.ga = (const char*)es.kv8;
+    a.gb = nullptr;
+    a.rb = (uint32_t)es.kv8_row;
+    a.kvref = es.kvref;
+  }
+  if (range.fill && !w.empty.empty())
     GT_TRY(pipe::fill_empty(pass, w.d_empty.as<int32_t>(), (int64_t)w.empty.size(), (char*)out_a, (char*)out_b,
                             out_f, (int64_t)P->heads * P->d * (P->dtype == GT_F32 ? 4 : 2), P->heads,
                             (int)P->st_row_bytes, st));

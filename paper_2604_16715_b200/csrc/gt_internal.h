@@ -235,6 +235,11 @@ struct gt_plan_s {
   gt::DevBuf h2d[9];
   cudaStream_t e2e_in = nullptr, e2e_out = nullptr;
   cudaEvent_t e2e_ev[5] = {}, ev_dq = nullptr;
+  // streamed world-1 gt_attn_fwd_bwd_host: C row (column) chunks - item bounds t, row bounds r, heavy-id
+  // bounds h of the row list [0] and the column list [1] - and one event per chunk and stage
+  int e2e_c = 0;
+  std::vector<int64_t> e2e_t[2], e2e_r[2], e2e_h[2];
+  std::vector<cudaEvent_t> e2e_cev;
   cudaEvent_t ev_dq_ready = nullptr;  // when set, gt_attn_bwd records it once dQ is complete
 
   // CUDA-graph replay (gt_opts.cuda_graphs, world 1): executable graphs keyed by the tensor pointers
@@ -255,6 +260,11 @@ struct gt_plan_s {
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t take_event();
+  // fp8 K||V storage (gt_opts.kv_fp8): quantised table, its row bytes, {E_k, E_v}, and the k, v it holds
+  bool kv_fp8 = false;
+  gt::DevBuf d_kv8, d_kvref;
+  int64_t kv8_row = 0;
+  const void* kv8_tag[2] = {nullptr, nullptr};
   nvtxRangeId_t nvtx_id[5] = {0, 0, 0, 0, 0};   // open NVTX range per stage
   void mark_begin(int stage, cudaStream_t st, cudaEvent_t* a);
   void mark_end(int stage, cudaStream_t st, cudaEvent_t a);
@@ -273,6 +283,9 @@ gt_status launch_fwd_peer(gt_plan_s* P, const void* q, const void* k, const void
                           cudaStream_t st);
 // use_logits: read the forward's stored logits (false: recompute q.k; the stored ones belong to
 // another forward)
+gt_status launch_pass_range(gt_plan_s* P, int pass, const void* q, const void* k, const void* v, const void* y,
+                            const float* lse, const void* dy, void* out_a, void* out_b, cudaStream_t st, int64_t t0,
+                            int64_t t1, int64_t h0, int64_t h1, bool fill);
 gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const void* y,
                           const void* halo_kv, const float* lse, const void* dy, void* dq, cudaStream_t st,
                           bool use_logits = true);
@@ -298,11 +311,23 @@ struct EntryState {
   int64_t nnbr = 0;
   int64_t own_stride = 0;        // bytes between own rows (0: one feature row)
   const void* own_c = nullptr;   // rowb: Y (D_i = <dY_i, Y_i>)
+  // fp8 K||V gathers (gt_opts.kv_fp8): the quantised table, its row bytes and {E_k, E_v}
+  const void* kv8 = nullptr;
+  int64_t kv8_row = 0;
+  const int* kvref = nullptr;
+};
+gt_status quantize_kv(int H, int D, const void* k, const void* v, int64_t n, void* out, int gr, int* ref,
+                      cudaStream_t st);
+// Item range [t0, t1) of the work list (t1 < 0: to its end); fill: also write the outputs of the list's
+// rows (columns) without entries.
+struct ItemRange {
+  int64_t t0 = 0, t1 = -1;
+  bool fill = true;
 };
 gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable& ct, float* part, const void* own_a,
                     const void* own_b, const float* lse, const void* gather_a, const void* gather_b, const void* halo,
                     const void* halo_s, void* out_a, void* out_b, float* out_f, cudaStream_t st, int reserve_sms,
-                    const EntryState& es = EntryState());
+                    const EntryState& es = EntryState(), const ItemRange& range = ItemRange());
 
 // pack kernels (comm.cu)
 gt_status pack_kv(const void* k, const void* v, const int32_t* idx, int64_t rows, int64_t D, int elt,

@@ -21,7 +21,7 @@ STRATEGIES = {"auto": GT_AUTO, "single": GT_SINGLE, "allgather": GT_ALLGATHER, "
 STRATEGY_NAMES = {v: k for k, v in STRATEGIES.items()}
 GT_COMM_NONE, GT_COMM_NCCL, GT_COMM_LOOPBACK, GT_COMM_HOSTIPC = range(4)
 EXPORT = {"bounds": 0, "halo_out": 1, "halo_in": 2, "send_out": 3, "send_in": 4, "csc_ptr": 5, "csc_idx": 6,
-          "heavy_rows": 7, "heavy_cols": 8}
+          "heavy_rows": 7, "heavy_cols": 8, "kv8": 9}
 _EXPORT_I64 = {"bounds", "csc_ptr"}
 
 
@@ -41,7 +41,7 @@ class _Opts(ctypes.Structure):
                 ("validate", ctypes.c_int), ("partition", ctypes.c_int), ("device", ctypes.c_int),
                 ("heavy_threshold", ctypes.c_int), ("beta_profile", ctypes.c_char_p), ("profile", ctypes.c_int),
                 ("edge_state", ctypes.c_int), ("bwd_mode", ctypes.c_int), ("transport", ctypes.c_int),
-                ("cuda_graphs", ctypes.c_int)]
+                ("cuda_graphs", ctypes.c_int), ("kv_fp8", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -56,7 +56,8 @@ class _Info(ctypes.Structure):
                    ("agp_score", ctypes.c_double * 5), ("agp_feasible", ctypes.c_int * 5),
                    ("alpha_s_per_unit", ctypes.c_double), ("edge_state", ctypes.c_int),
                    ("edge_state_bytes", ctypes.c_int64), ("bwd_mode", ctypes.c_int),
-                   ("transport", ctypes.c_int), ("fwd_gen", ctypes.c_int64), ("stale_bwds", ctypes.c_int64)])
+                   ("transport", ctypes.c_int), ("fwd_gen", ctypes.c_int64), ("stale_bwds", ctypes.c_int64),
+                   ("kv_fp8", ctypes.c_int), ("kv_fp8_bytes", ctypes.c_int64)])
 
 
 _lib = None
@@ -314,13 +315,14 @@ class Plan:
     (materialised logits and (P, dP): auto / on / off); bwd_mode 0 (transposed owner) | 1
     (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); cuda_graphs (world-1 graph
     replay); beta_profile (JSON of measured beta per strategy for GT_AUTO instead of plan-time probes);
-    profile (per-stage CUDA events).
+    profile (per-stage CUDA events); kv_fp8 (fp8 K||V storage, gt_opts.kv_fp8: world 1, bf16, entry state).
     """
 
     def __init__(self, row_ptr, col_idx, heads: int, d: int, dtype="bf16", scale: float = 0.0, world: int = 1,
                  rank: int = 0, comm=None, strategy="auto", heavy_threshold: int = 0, partition: int = 0,
                  validate: bool = True, device: int = -1, profile: bool = False, edge_state: int = 0,
-                 bwd_mode: int = 0, transport: int = 0, cuda_graphs: bool = False, beta_profile=None):
+                 bwd_mode: int = 0, transport: int = 0, cuda_graphs: bool = False, beta_profile=None,
+                 kv_fp8: bool = False):
         L = lib()
         self.row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         self.col_idx = np.ascontiguousarray(col_idx, np.int32)
@@ -341,6 +343,7 @@ class Plan:
         opts.bwd_mode = int(bwd_mode)
         opts.transport = int(transport)
         opts.cuda_graphs = int(cuda_graphs)
+        opts.kv_fp8 = int(kv_fp8)
         self._beta_profile = str(beta_profile).encode() if beta_profile else None  # kept alive for gt_plan
         opts.beta_profile = self._beta_profile
         if world > 1:
@@ -381,7 +384,7 @@ class Plan:
         code = EXPORT[what]
         ln = _I64()
         _check(lib().gt_plan_export(self.handle, code, peer, None, 0, ctypes.byref(ln)))
-        dt = np.int64 if what in _EXPORT_I64 else np.int32
+        dt = np.int64 if what in _EXPORT_I64 else (np.uint8 if what == "kv8" else np.int32)
         out = np.zeros(max(ln.value, 1), dt)
         _check(lib().gt_plan_export(self.handle, code, peer, out.ctypes.data, ln.value, ctypes.byref(ln)))
         return out[:ln.value]

@@ -4,9 +4,9 @@
 //   stream : ld.global.cg.v4 (16 B per thread), 4 independent loads in flight per thread;
 //   gather : the hot kernels' pattern - each warp copies whole 512-byte rows picked by a hash of
 //            (warp, iteration) with cp.async.cg 16 B per lane into a shared-memory ring (4 rows per
-//            stage, 2 stages), one commit group per stage;
-//   bulk   : cp.async.bulk (TMA) of 4 KB chunks into shared memory, one elected lane per warp.
-// Prints one JSON object per mode: bytes read / CUDA-event time, best of `reps` launches.
+//            stage, 2 stages), one commit group per stage, at 4..12 resident CTAs of 4 warps per SM.
+// Prints one JSON object per mode: bytes read / CUDA-event time, best of `reps` launches, next to the
+// SM-ingress figure 64 B/clk/SM x SMs x the current SM clock.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/l2bw tools/l2bw.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -103,10 +103,14 @@ int main(int argc, char** argv) {
            cudaGetErrorString(e));
   }
   // gather (the kernels' access pattern), at several resident-warp counts
-  for (int ctas = 4; ctas <= 8; ctas += 2) {
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  printf("{\"mode\": \"sm_ingress_64B_per_clk\", \"l2_read_gbs\": %.1f, \"sm_clock_mhz\": %.0f}\n",
+         64.0 * sms * clk_khz * 1e3 / 1e9, clk_khz / 1e3);
+  for (int ctas = 4; ctas <= 12; ctas += 2) {
     const int grid = sms * ctas, smem = 4 * 2 * 4 * 512;
     const uint32_t rows = (uint32_t)(bytes / 512);
-    const int iters = (int)((int64_t)passes * rows / 4 / ((int64_t)grid * 4)) + 1;
+    const int iters = (int)((int64_t)passes * rows / 4 / ((int64_t)grid * 4)) + 1;  // passes over the table
     gather_rd<<<grid, 128, smem>>>(p, rows, 64, sink);
     float best = 1e30f;
     for (int r = 0; r < reps; ++r) {
