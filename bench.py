@@ -46,6 +46,8 @@ def parse():
                     help="gt_opts.bwd_mode (world > 1): 0 transposed owner, 1 reduce-scatter of fp32 partials")
     ap.add_argument("--kv-fp8", type=int, default=int(os.environ.get("GT_KV_FP8", "0")),
                     help="gt_opts.kv_fp8: fp8 K||V storage (NEXT-4 option; not the bf16 headline)")
+    ap.add_argument("--hot-cols", type=int, default=int(os.environ.get("GT_HOT_COLS", "0")),
+                    help="gt_opts.hot_cols: hot-column K||V table in persisting L2 (world 1)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -429,7 +431,7 @@ def run_ours(args):
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
                    strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local,
                    edge_state=args.edge_state, bwd_mode=args.bwd_mode, transport=args.transport,
-                   kv_fp8=bool(args.kv_fp8))
+                   kv_fp8=bool(args.kv_fp8), hot_cols=args.hot_cols if world == 1 else 0)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     info = plan.info()
@@ -547,7 +549,8 @@ def run_ours(args):
                        "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 512,
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
                        "bwd_mode": info["bwd_mode"], "transport": info["transport"],
-                       "kv_fp8": info["kv_fp8"]},
+                       "kv_fp8": info["kv_fp8"], "hot_cols": info["hot_cols"],
+                       "hot_entries": info["hot_entries"]},
             "roofline": roofline,
             # whole step: ncu DRAM bytes of the three passes over the step time (physical), and the
             # no-reuse gather model (exceeds 1 on L2-local graphs: a model, not a fraction of the peak)

@@ -163,6 +163,15 @@ typedef struct {
                               not the last forward's re-quantises them.  Needs world == 1, a bf16
                               plan, heads * d >= 128 and the materialised entry state (edge_state
                               >= 0 and fitting); else GT_ECONFIG.  0 => K, V gathered as given. */
+  int hot_cols;            /* > 0 => hot-column table (world 1; not with kv_fp8): the K || V rows of the
+                              hot_cols columns with the most entries (power-law hubs, e.g. R-MAT) are
+                              packed by every gt_attn_fwd into one contiguous plan table that the
+                              forward and row-pass kernels read under an L2 access-policy window
+                              (persisting), and the plan's CSR entries of those columns point into
+                              it.  Sets the device's persisting-L2 limit.  Results are unchanged
+                              (the same values are read).  Measured slower on the C3 / C5
+                              benchmarks: an option for graphs whose hubs LRU
+                              evicts.  0 => off. */
 } gt_opts;
 
 typedef struct {
@@ -194,6 +203,8 @@ typedef struct {
                                      gt_attn_fwd (they re-fetched / recomputed the forward's state) */
   int kv_fp8;                     /* 1 if K, V are gathered from the plan's fp8 table (gt_opts.kv_fp8) */
   int64_t kv_fp8_bytes;           /* device bytes of that table */
+  int64_t hot_cols;               /* columns in the hot-column table (gt_opts.hot_cols) */
+  int64_t hot_entries;            /* owned-row entries that read it */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,

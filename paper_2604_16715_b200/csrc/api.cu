@@ -378,6 +378,9 @@ static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
   I.kv_fp8 = P->kv_fp8 ? 1 : 0;
   I.kv_fp8_bytes = P->kv_fp8 ? P->n_local * P->kv8_row : 0;
   if (P->kv_fp8) I.launches_fwd += 1;                   // + the quantisation
+  I.hot_cols = P->n_hot;
+  I.hot_entries = P->hot_entries;
+  if (P->n_hot) I.launches_fwd += 1;                    // + the hot-table pack
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
@@ -385,7 +388,7 @@ static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
                           &P->d_hrow, &P->d_hsrc, &P->d_part_h, &P->d_rs_send, &P->d_part_rs, &P->d_mptr, &P->d_midx,
                           &P->d_hq, &P->d_hk, &P->d_hv, &P->d_hy, &P->d_hlse, &P->d_hdy, &P->d_hdq, &P->d_hdk,
                           &P->d_hdv, &P->d_stage[0], &P->d_stage[1], &P->d_stage[2], &P->d_pub, &P->d_iota, &P->d_pub_qd,
-                          &P->d_kv8, &P->d_kvref})
+                          &P->d_kv8, &P->d_kvref, &P->d_hot, &P->d_hot_idx})
     dev += (int64_t)b->bytes;
   if (P->strategy == GT_A2A && P->sub) {  // the world-1 plan over all rows with heads / world heads
     const gt_plan_info& S = P->sub->info;
@@ -495,6 +498,9 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     return fail(GT_ECONFIG, "gt_plan: the peer-gather transport needs world <= 8 and the transposed-owner backward");
   if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
   if (opts->kv_fp8 != 0 && opts->kv_fp8 != 1) return fail(GT_EINVAL, "gt_plan: kv_fp8 must be 0 or 1");
+  if (opts->hot_cols < 0) return fail(GT_EINVAL, "gt_plan: hot_cols must be >= 0");
+  if (opts->hot_cols > 0 && (world != 1 || opts->kv_fp8))
+    return fail(GT_ECONFIG, "gt_plan: hot_cols needs world == 1 and kv_fp8 == 0");
   if (opts->kv_fp8 && (world != 1 || opts->dtype != GT_BF16 || (int64_t)heads * d < 128 || opts->edge_state < 0))
     return fail(GT_ECONFIG, "gt_plan: kv_fp8 needs world == 1, a bf16 plan, heads * d >= 128 and the entry state");
   if (opts->validate) GT_TRY(validate_csr(csr->row_ptr, csr->col_idx, n, nnz));
@@ -746,6 +752,37 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
     P->strategy = strategy;
   } else {
     P->strategy = GT_SINGLE;
+    // ---- hot-column table (opts.hot_cols): the K||V rows of the most referenced columns, packed per
+    // forward and read under a persisting L2 access-policy window; their CSR entries point into it ----
+    if (opts->hot_cols > 0 && nnz > 0) {
+      const int64_t H = std::min<int64_t>(opts->hot_cols, n);
+      std::vector<int32_t> order((size_t)n);
+      std::iota(order.begin(), order.end(), 0);
+      std::partial_sort(order.begin(), order.begin() + H, order.end(), [&](int32_t a, int32_t b) {
+        const int64_t da = col_ptr_full[a + 1] - col_ptr_full[a], db = col_ptr_full[b + 1] - col_ptr_full[b];
+        return da != db ? da > db : a < b;
+      });
+      order.resize((size_t)H);
+      std::vector<int32_t> slot((size_t)n, -1);
+      for (int64_t x = 0; x < H; ++x) slot[(size_t)order[(size_t)x]] = (int32_t)x;
+      std::vector<int32_t> cols((size_t)nnz);
+      int64_t hits = 0;
+      for (int64_t e = 0; e < nnz; ++e) {
+        const int32_t j = csr->col_idx[e], sl = slot[(size_t)j];
+        cols[(size_t)e] = sl >= 0 ? (int32_t)(n + sl) : j;
+        hits += sl >= 0;
+      }
+      GT_TRY(upload(P->d_col, cols.data(), cols.size()));
+      GT_TRY(upload(P->d_hot_idx, order.data(), order.size()));
+      GT_TRY(P->d_hot.alloc((size_t)H * P->kv_row_bytes));
+      P->n_hot = H;
+      P->hot_entries = hits;
+      int maxp = 0;
+      GT_CUDA_TRY(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, P->device));
+      if (maxp > 0)
+        GT_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                       (size_t)std::min<int64_t>(maxp, (int64_t)P->d_hot.bytes)));
+    }
   }
   if (P->strategy == GT_A2A) {
     GT_TRY(build_a2a(P.get(), csr, n, nnz, d, opts));
@@ -1141,6 +1178,15 @@ static gt_status requantize(gt_plan_t P, const void* k, const void* v, cudaStrea
   return GT_OK;
 }
 
+// hot-column table (gt_opts.hot_cols) of these k, v
+static gt_status repack_hot(gt_plan_t P, const void* k, const void* v, cudaStream_t st) {
+  GT_TRY(pack_kv(k, v, P->d_hot_idx.as<int32_t>(), P->n_hot, (int64_t)P->heads * P->d, P->dtype == GT_F32 ? 4 : 2,
+                 P->d_hot.p, st));
+  P->hot_tag[0] = k;
+  P->hot_tag[1] = v;
+  return GT_OK;
+}
+
 static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const void* v, void* y, float* lse,
                                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -1178,6 +1224,10 @@ static gt_status attn_fwd_eager(gt_plan_t P, const void* q, const void* k, const
   }
   P->mark_begin(1, st, &ev);
   if (P->kv_fp8) GT_TRY(requantize(P, k, v, st));
+  if (P->n_hot) {
+    GT_TRY(repack_hot(P, k, v, st));
+    halo = P->d_hot.p;
+  }
   GT_TRY(launch_fwd(P, q, k, v, halo, y, lse, st, P->world > 1 ? P->ev_halo : nullptr));
   P->mark_end(1, st, ev);
   set_fwd_tag(P, q, k, v, lse);
@@ -1225,8 +1275,13 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     P->mark_end(3, st, e1);
     return GT_OK;
   }
-  // remote K || V rows: the received table, or (peer gather) the owners' published rows
-  const void* halo_kv = P->world > 1 ? (P->peer ? P->d_pub.p : P->d_recv_kv.p) : nullptr;
+  // remote K || V rows: the received table, or (peer gather) the owners' published rows; world 1 with
+  // gt_opts.hot_cols: the hot-column table (re-packed when it holds another forward's k, v)
+  const void* halo_kv = P->world > 1 ? (P->peer ? P->d_pub.p : P->d_recv_kv.p) : (P->n_hot ? P->d_hot.p : nullptr);
+  if (P->n_hot && (P->hot_tag[0] != k || P->hot_tag[1] != v)) {
+    GT_TRY(repack_hot(P, k, v, st));
+    if (!fresh) stale = true;
+  }
   cudaEvent_t ev = nullptr, ev2 = nullptr;
   const bool multi = P->world > 1;
   const bool ag = P->strategy == GT_ALLGATHER;
@@ -1491,6 +1546,7 @@ static gt_status fwd_bwd_host_streamed(gt_plan_t P, const void* q, const void* k
   // forward, in row chunks
   GT_CUDA_TRY(cudaStreamWaitEvent(st, ev_kv, 0));
   if (P->kv_fp8) GT_TRY(requantize(P, dk_, dv_, st));
+  if (P->n_hot) GT_TRY(repack_hot(P, dk_, dv_, st));
   for (int c = 0; c < Cr; ++c) {
     GT_CUDA_TRY(cudaStreamWaitEvent(st, ev[c], 0));
     GT_TRY(launch_pass_range(P, 0, dq_, dk_, dv_, nullptr, dl, nullptr, dy_, nullptr, st, P->e2e_t[0][c],

@@ -306,6 +306,10 @@ int launches_bwd(const gt_plan_s* P) {
 // logits in the same order, the column pass reads (P, dP) through the CSC -> CSR map.
 static EntryState entry_state(gt_plan_s* P, int pass, bool use_logits = true) {
   EntryState e;
+  if (P->n_hot && pass < 2) {  // hot-column table read under a persisting L2 window (gt_opts.hot_cols)
+    e.win = P->d_hot.p;
+    e.win_bytes = (int64_t)P->d_hot.bytes;
+  }
   if (!P->es) return e;
   if (P->kv_fp8 && pass < 2) {  // fp8 K||V gathers (gt_opts.kv_fp8)
     e.kv8 = P->d_kv8.p;
@@ -412,13 +416,14 @@ gt_status launch_pass_range(gt_plan_s* P, int pass, const void* q, const void* k
   const ItemRange rg{t0, t1, fill};
   const ChunkTable& ct = pass == 2 ? P->heavy_cols : P->heavy_rows;
   const DevBuf& part = pass == 0 ? P->d_part_fwd : (pass == 1 ? P->d_part_rowb : P->d_part_colb);
+  const void* hot = P->n_hot ? P->d_hot.p : nullptr;  // hot-column table (gt_opts.hot_cols)
   if (pass == 0) {
-    GT_TRY(pipe_pass(P, 0, P->w_rows, ct, part.as<float>(), q, nullptr, nullptr, k, v, nullptr, nullptr, out_a,
+    GT_TRY(pipe_pass(P, 0, P->w_rows, ct, part.as<float>(), q, nullptr, nullptr, k, v, hot, nullptr, out_a,
                      nullptr, const_cast<float*>(lse), st, 0, entry_state(P, 0), rg));
   } else if (pass == 1) {
     EntryState e = entry_state(P, 1, true);
     e.own_c = y;
-    GT_TRY(pipe_pass(P, 1, P->w_rows, ct, part.as<float>(), q, dy, lse, k, v, nullptr, nullptr, out_a, nullptr,
+    GT_TRY(pipe_pass(P, 1, P->w_rows, ct, part.as<float>(), q, dy, lse, k, v, hot, nullptr, out_a, nullptr,
                      P->d_stats.as<float>(), st, 0, e, rg));
   } else {
     GT_TRY(pipe_pass(P, 2, P->w_cols, ct, part.as<float>(), k, v, nullptr, q, dy, nullptr, nullptr, out_a, out_b,

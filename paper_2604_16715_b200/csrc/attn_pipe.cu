@@ -245,6 +245,8 @@ struct PArgs {
   const float* es_in;    // rowb: s2 | colb: (P, dS)
   const int32_t* src;    // colb: local CSC position -> local CSR entry (read through a window like nbr)
   const int* kvref;      // fp8 gathers: {E_k, E_v} = max exponent of the K / V scales over the table
+  const void* win;       // persisting L2 access-policy window of the launch (hot-column table), or null
+  int64_t win_bytes;
   uint32_t rb, rb2, sb;  // row strides (bytes) of the gathered tables as run-time values: a row address is
                          // then one IMAD.WIDE.U32 (an immediate power-of-two stride becomes shift + high +
                          // two 64-bit adds)
@@ -1467,6 +1469,24 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
     GT_TRY(encode_rows(&tm.b, a.gb, a.n_local, D, (int)sizeof(T), C::RB));
   }
   GT_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(unsigned long long), st));
+  if (a.win && a.win_bytes > 0) {  // hot-column table: persisting in L2 for this launch
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(a.win);
+    at[0].val.accessPolicyWindow.num_bytes = (size_t)a.win_bytes;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    GT_CUDA_TRY(cudaLaunchKernelEx(&cfg, pipe_kernel<T, H, D, PASS, HALO, ES>, a, tm));
+    return GT_OK;
+  }
   pipe_kernel<T, H, D, PASS, HALO, ES><<<g, kWarps * 32, smem, st>>>(a, tm);
   GT_CUDA_TRY(cudaGetLastError());
   return GT_OK;
@@ -1579,6 +1599,8 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.es_out = es.out;
   a.es_in = es.in;
   a.src = es.src;
+  a.win = es.win;
+  a.win_bytes = es.win_bytes;
   if (es.kv8 && pass < 2) {  // fp8 K||V table replaces the two gathered tables
     a.ga = (const char*)es.kv8;
     a.gb = nullptr;

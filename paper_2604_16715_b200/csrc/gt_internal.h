@@ -265,6 +265,10 @@ struct gt_plan_s {
   gt::DevBuf d_kv8, d_kvref;
   int64_t kv8_row = 0;
   const void* kv8_tag[2] = {nullptr, nullptr};
+  // hot-column table (gt_opts.hot_cols, world 1): packed [k | v] rows of the top in-degree columns
+  int64_t n_hot = 0, hot_entries = 0;
+  gt::DevBuf d_hot, d_hot_idx;
+  const void* hot_tag[2] = {nullptr, nullptr};
   nvtxRangeId_t nvtx_id[5] = {0, 0, 0, 0, 0};   // open NVTX range per stage
   void mark_begin(int stage, cudaStream_t st, cudaEvent_t* a);
   void mark_end(int stage, cudaStream_t st, cudaEvent_t a);
@@ -311,6 +315,9 @@ struct EntryState {
   int64_t nnbr = 0;
   int64_t own_stride = 0;        // bytes between own rows (0: one feature row)
   const void* own_c = nullptr;   // rowb: Y (D_i = <dY_i, Y_i>)
+  // L2 access-policy window (persisting) for the launch: the hot-column table (gt_opts.hot_cols)
+  const void* win = nullptr;
+  int64_t win_bytes = 0;
   // fp8 K||V gathers (gt_opts.kv_fp8): the quantised table, its row bytes and {E_k, E_v}
   const void* kv8 = nullptr;
   int64_t kv8_row = 0;

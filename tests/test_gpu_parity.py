@@ -196,6 +196,44 @@ def test_host_buffer_streamed_chunks(gt, chunks, monkeypatch):
     plan.close()
 
 
+@pytest.mark.parametrize("dtype,h,d", [("bf16", 4, 64), ("f32", 8, 16)])
+def test_hot_column_table(gt, dtype, h, d):
+    """gt_opts.hot_cols: the most referenced columns' K||V rows are read from a packed table under a
+    persisting L2 window; outputs are the oracle's, through the device API (incl. a backward of another
+    forward's k, v, which re-packs) and the streamed host-buffer step."""
+    import torch
+    rp, ci = gtgen.random_graph(3000, 45000, seed=64, directed=True, power=1.9)
+    n = len(rp) - 1
+    A = inputs(n, h, d, dtype, 641)
+    B = inputs(n, h, d, dtype, 642, qk_scale=3.0)
+    plan = gt.Plan(rp, ci, h, d, dtype=dtype, heavy_threshold=64, hot_cols=200)
+    info = plan.info()
+    indeg = np.bincount(ci, minlength=n)
+    assert info["hot_cols"] == 200 and info["hot_entries"] == np.sort(indeg)[-200:].sum()
+    ta, tb = [to_torch(x) for x in A], [to_torch(x) for x in B]
+    ya, la = plan.fwd(*ta[:3])
+    yb, lb = plan.fwd(*tb[:3])
+    ga = plan.bwd(*ta[:3], ya, la, ta[3])      # the table holds B's rows: re-packed
+    torch.cuda.synchronize()
+    for X, (y, l, g) in ((A, (ya, la, ga)), (B, (yb, lb, None))):
+        Y, LSE = oracle.forward(rp, ci, *X[:3], plan.scale)
+        assert normwise(to_f64(y), Y) <= TOL[dtype]
+        check_lse(to_f64(l), LSE, dtype)
+        if g is not None:
+            DQ, DK, DV, _ = oracle.backward(rp, ci, *X, plan.scale)
+            for a, r in zip(g, (DQ, DK, DV)):
+                assert normwise(to_f64(a), r) <= TOL[dtype]
+    pin = lambda x: to_torch(x, "cpu").pin_memory()  # noqa: E731
+    hq, hk, hv, hdy = (pin(x) for x in B)
+    outs = [torch.empty_like(hq).pin_memory() for _ in range(4)]
+    hl = torch.empty((n, h), dtype=torch.float32).pin_memory()
+    plan.fwd_bwd_host(hq, hk, hv, hdy, outs[0], hl, outs[1], outs[2], outs[3])
+    DQ, DK, DV, _ = oracle.backward(rp, ci, *B, plan.scale)
+    for a, r in zip(outs[1:], (DQ, DK, DV)):
+        assert normwise(to_f64(a), r) <= TOL[dtype]
+    plan.close()
+
+
 def test_errors_are_reported(gt):
     rp, ci = gtgen.csr_from_pairs(4, [(0, 1), (1, 2)])
     bad = ci.copy()
