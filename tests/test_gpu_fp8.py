@@ -105,6 +105,37 @@ def test_fp8_stale_backward_requantises():
     plan.close()
 
 
+@pytest.mark.parametrize("case", ["empty", "hub", "zero_rows"])
+def test_fp8_degenerate(case):
+    """fp8 on graphs without entries, with one hub row / column, and with all-zero K / V rows (scale
+    exponent -126, codes 0) next to ordinary ones."""
+    import torch
+    import paper_2604_16715_b200 as gt
+    h, d = 4, 64
+    if case == "empty":
+        rp, ci = np.zeros(50, np.int64), np.zeros(0, np.int32)
+    elif case == "hub":
+        n = 500
+        rp, ci = gtgen.csr_from_pairs(n, [(0, j) for j in range(1, n)] + [(j, 0) for j in range(1, n)])
+    else:
+        rp, ci = gtgen.random_graph(800, 9000, seed=81, directed=True, power=2.2)
+    n = len(rp) - 1
+    q, k, v, dy = inputs(n, h, d, "bf16", 811)
+    if case == "zero_rows":
+        k[::7] = 0
+        v[::5, 1] = 0
+    scale = 1.0 / math.sqrt(h * d)
+    plan = gt.Plan(rp, ci, h, d, dtype="bf16", scale=scale, heavy_threshold=64, kv_fp8=True)
+    tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
+    y, lse = plan.fwd(tq, tk, tv)
+    dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
+    torch.cuda.synchronize()
+    if n:
+        np.testing.assert_array_equal(plan.export("kv8").reshape(n, -1), table_reference(k, v, h))
+    check_all([to_f64(t) for t in (y, lse, dq, dk, dv)], reference(rp, ci, q, k, v, dy, scale), case)
+    plan.close()
+
+
 def test_fp8_config_errors():
     import paper_2604_16715_b200 as gt
     rp, ci = gtgen.random_graph(300, 2000, seed=5, power=2.3)

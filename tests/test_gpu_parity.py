@@ -196,6 +196,36 @@ def test_host_buffer_streamed_chunks(gt, chunks, monkeypatch):
     plan.close()
 
 
+@pytest.mark.parametrize("case", ["empty", "one_hub", "single_edge"])
+def test_host_buffer_streamed_degenerate(gt, case, monkeypatch):
+    """The streamed host path on graphs with no entries, one hub row / column carrying every entry
+    (a single chunked row: no row-chunk cut exists), and one edge among isolated nodes."""
+    import torch
+    monkeypatch.setenv("GT_E2E_CHUNKS", "8")
+    if case == "empty":
+        rp, ci = np.zeros(40, np.int64), np.zeros(0, np.int32)
+    elif case == "one_hub":
+        n = 600
+        rp, ci = gtgen.csr_from_pairs(n, [(0, j) for j in range(1, n)] + [(j, 0) for j in range(1, n)])
+    else:
+        rp, ci = gtgen.csr_from_pairs(9, [(4, 7)])
+    n, h, d = len(rp) - 1, 4, 64
+    q, k, v, dy = inputs(n, h, d, "bf16", 607)
+    plan = gt.Plan(rp, ci, h, d, dtype="bf16", heavy_threshold=64)
+    pin = lambda x: to_torch(x, "cpu").pin_memory()  # noqa: E731
+    tq, tk, tv, tdy = (pin(x) for x in (q, k, v, dy))
+    y, dq, dk, dv = (torch.full_like(tq, float("nan")).pin_memory() for _ in range(4))
+    lse = torch.full((n, h), float("nan"), dtype=torch.float32).pin_memory()
+    plan.fwd_bwd_host(tq, tk, tv, tdy, y, lse, dq, dk, dv)
+    Y, LSE = oracle.forward(rp, ci, q, k, v, plan.scale)
+    DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, plan.scale)
+    for a, r in ((y, Y), (dq, DQ), (dk, DK), (dv, DV)):
+        assert not torch.isnan(a.float()).any()
+        assert normwise(to_f64(a), r) <= 2e-2
+    check_lse(lse.numpy(), LSE, "bf16")
+    plan.close()
+
+
 @pytest.mark.parametrize("dtype,h,d", [("bf16", 4, 64), ("f32", 8, 16)])
 def test_hot_column_table(gt, dtype, h, d):
     """gt_opts.hot_cols: the most referenced columns' K||V rows are read from a packed table under a
