@@ -71,7 +71,13 @@ constexpr int kMaxDevices = 64;
 #define GT_PIPE_TMA 0  // measured slower on C3; kept for A/B builds
 #endif
 constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
-constexpr int kS = GT_PIPE_STAGES;      // stages per warp (2 measured best: more resident warps)
+#ifndef GT_COLB_STAGES
+#define GT_COLB_STAGES 2
+#endif
+// stages per warp: 2 (measured best: more resident warps).  A third stage for the stored-state column
+// pass alone measured 8.45 -> 8.54 ms on C3 (3 stages for every pass: column pass -4 %, row pass +15 %)
+template <int PASS, int ES>
+constexpr int stages_of() { return (PASS == 2 && (ES & 1)) ? GT_COLB_STAGES : GT_PIPE_STAGES; }
 constexpr int kG = GT_PIPE_GRAB;        // items per grab
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -195,6 +201,7 @@ struct PC {
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
   // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dS)[U][H]
   static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0);
+  static constexpr int kS = stages_of<PASS, ES>();                   // stages per warp
   static constexpr int MB = TMA ? kS * 8 : 0;                       // one mbarrier per stage
   static constexpr int WARP_SMEM = (kS * (STAGE + OWNP + XS) + MB + 127) / 128 * 128;
   // byte offsets in a stage of neighbour u's first row, second row and (LSE2, D) block (tma: the kernel
@@ -625,11 +632,11 @@ struct Meta {      // warp-uniform description of one filled stage
 #ifndef GT_COLB_MINB
 #define GT_COLB_MINB 1
 #endif
-#ifndef GT_FWD_MINB
-#define GT_FWD_MINB 1
+#ifndef GT_FWD_MINB  // forward: 6 CTAs/SM (<= 80 registers, no spills) with the full shared-memory carveout
+#define GT_FWD_MINB 6
 #endif
 #ifndef GT_CARVEOUT  // preferred shared-memory carveout (percent of the unified L1/shared array); -1 = driver's
-#define GT_CARVEOUT -1
+#define GT_CARVEOUT 100
 #endif
 template <int PASS, int ES, int EPL>
 constexpr int min_ctas() {
@@ -654,6 +661,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int head = lane / LPH;
+  constexpr int kS = C::kS;
   char* const stages = smem + (size_t)wid * C::WARP_SMEM;   // kS * STAGE
   char* const owns = stages + kS * C::STAGE;                 // kS * OWNP
   char* const xs = owns + kS * C::OWNP;                      // kS * XS
