@@ -317,10 +317,10 @@ def oracle_step(sub_rp, sub_ci, R, cfg, seed, scale, keep=False):
     import oracle
     q, k, v, dy = (gtgen.features(seed, nm, R, cfg.heads, cfg.d, cfg.dtype) for nm in ("q", "k", "v", "dy"))
     t0 = time.perf_counter()
-    Y, _ = oracle.forward(sub_rp, sub_ci, q, k, v, scale)
+    Y, LSE = oracle.forward(sub_rp, sub_ci, q, k, v, scale)
     DQ, DK, DV, _ = oracle.backward(sub_rp, sub_ci, q, k, v, dy, scale)
     t = time.perf_counter() - t0
-    return (t, (q, k, v, dy), (Y, DQ, DK, DV)) if keep else t
+    return (t, (q, k, v, dy), (Y, DQ, DK, DV, LSE)) if keep else t
 
 
 def sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs):
@@ -336,7 +336,12 @@ def sample_parity(gt, sub_rp, sub_ci, cfg, scale, feats, refs):
     dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
     torch.cuda.synchronize()
     out, elem = {}, {}
-    for name, got, ref in zip(("y", "dq", "dk", "dv"), (y, dq, dk, dv), refs):
+    L = lse.to(torch.float64).cpu().numpy()
+    LREF = refs[4]
+    fin = np.isfinite(LREF)
+    out["lse_abs_err"] = float(np.max(np.abs(L[fin] - LREF[fin]))) if fin.any() else 0.0
+    out["lse_empty_rows_match"] = bool(np.array_equal(np.isneginf(L), np.isneginf(LREF)))
+    for name, got, ref in zip(("y", "dq", "dk", "dv"), (y, dq, dk, dv), refs[:4]):
         g = got.to(torch.float64).cpu().numpy()
         den = float(np.max(np.abs(ref))) or 1.0
         out[name] = float(np.max(np.abs(g - ref)) / den)
@@ -534,7 +539,12 @@ def run_ours(args):
     if rank == 0:
         value = nnz / (ms * 1e-3)
         rep = report_fields(per_step, stages, info, world, nnz, step_bytes, peak)
+        rep["chosen_by_planner"] = (args.strategy or ("single" if world == 1 else "auto")) == "auto"
+        rep["ncu_dram_bytes"] = roofline.get("traffic")
+        rep["ncu_dram_gbs"] = roofline.get("achieved")
         if cpu:
+            rep["speedup_vs_oracle"] = value / cpu["value"]
+            rep["lse_abs_err"] = cpu["parity_normwise"].get("lse_abs_err")
             rep["max_rel_err"] = cpu["parity_normwise"]
             rep["bitexact_partition_halo"] = cpu["bitexact_partition_halo"]
             rep["oracle_threads"], rep["oracle_cpu"] = cpu["cores"], cpu["cpu_model"]
