@@ -34,7 +34,7 @@
  * world).
  *
  * Per-entry state (gt_opts.edge_state, on by default when it fits): the forward keeps each entry's
- * logit and the row pass its (P, dP) (Table 1 keeps Z and U per edge), so the
+ * logit and the row pass its (P, dS) (Table 1 keeps Z and U per edge), so the
  * backward does not recompute them.
  *
  * Conventions
@@ -127,7 +127,8 @@ typedef struct {
                               1 => materialise (GT_ENOMEM if it does not fit), -1 => never
                               (recompute q.k in the row pass, q.k and dY.v in the column pass).
                               Materialised, the forward stores base-2 logits (4 h B per owned-row
-                              entry), the row pass (P, dP) (8 h B per owned-row entry), both fp32,
+                              entry, fp32), the row pass (P, dS) (4 h B per owned-row entry as bf16x2 for bf16
+                              plans, 8 h B as fp32 pairs for fp32 plans),
                               and the plan holds a 4 B CSC -> CSR map per owned-column entry. */
   int bwd_mode;            /* world > 1 backward dataflow (reading Z11 of PAPER.md P:113):
                               0 => transposed owner: the owner of column j computes dK_j, dV_j after

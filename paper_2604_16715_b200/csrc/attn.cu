@@ -302,8 +302,8 @@ int launches_bwd(const gt_plan_s* P) {
 }
 
 // Entry-state arguments of a pass (Table 1 keeps Z and U per edge): the forward
-// stores base-2 logits and the row pass (P, dP) per entry in local CSR order; the row pass reads the
-// logits in the same order, the column pass reads (P, dP) through the CSC -> CSR map.
+// stores base-2 logits and the row pass (P, dS) per entry in local CSR order; the row pass reads the
+// logits in the same order, the column pass reads (P, dS) through the CSC -> CSR map.
 static EntryState entry_state(gt_plan_s* P, int pass, bool use_logits = true) {
   EntryState e;
   if (P->n_hot && pass < 2) {  // hot-column table read under a persisting L2 window (gt_opts.hot_cols)
@@ -463,7 +463,7 @@ gt_status launch_bwd_rows(gt_plan_s* P, const void* q, const void* k, const void
   return GT_OK;
 }
 
-// Column pass.  With entry state and world > 1 the owned-row entries (phase A, stored (P, dP)) run
+// Column pass.  With entry state and world > 1 the owned-row entries (phase A, stored (P, dS)) run
 // before `side_ready` (the in-halo [q | dy] rows and stats) is waited on; the remote-row entries
 // (phase B) recompute p and dP; columns split across the phases are merged.
 gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy,

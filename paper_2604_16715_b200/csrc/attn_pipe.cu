@@ -9,7 +9,7 @@
 //
 // Entry state (template bits ES; Table 1 keeps Z and U per edge): with bit 2 the
 // forward stores each entry's base-2 logit and the row pass reads it instead of q.k; with bit 1 the
-// row pass stores (p, dP) per entry and the column pass reads them (through the CSC -> CSR map)
+// row pass stores (p, dS) per entry and the column pass reads them (through the CSC -> CSR map)
 // instead of recomputing q.k and dY.v.  Stores go through a per-warp shared-memory transpose: one
 // coalesced, predicated store per stage.  Without entry state the column pass recomputes p and dP
 // from (q_i, dY_i, LSE_i, D_i) and its own k_j, v_j.
@@ -1502,7 +1502,7 @@ gt_status launch(const PArgs& a, cudaStream_t st, int reserve_sms) {
 
 template <typename T, int H, int D>
 struct Ops {
-  // ES bits: 1 = (P, dP) materialised (rowb stores, colb reads), 2 = logits materialised (fwd stores,
+  // ES bits: 1 = (P, dS) materialised (rowb stores, colb reads), 2 = logits materialised (fwd stores,
   // rowb reads)
   static gt_status run(int pass, const PArgs& a, cudaStream_t st, int rs) {
     if (a.kvref) {  // fp8 K||V gathers (world 1, bf16, heads * d >= 128)

@@ -5,7 +5,7 @@
 // the source row as value; the input is in CSR order (rows ascending), so stability leaves rows
 // ascending within each column -> the canonical CSC, unique given the edge set (bit-exact vs
 // the oracle's counting-sort transpose).  The sort carries the CSR entry index, so the same pass
-// yields the CSC -> CSR entry map through which the column pass reads the row pass's (P, dP).
+// yields the CSC -> CSR entry map through which the column pass reads the row pass's (P, dS).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>

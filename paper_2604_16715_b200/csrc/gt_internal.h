@@ -144,7 +144,7 @@ struct gt_plan_s {
   gt::DevBuf d_part_colb;          // [col chunks, 2 D]
 
   // materialised entry state (opts.edge_state; Table 1 stores U per edge): the row
-  // pass writes (P, dP) per entry in CSR order, and the column pass gathers them through the
+  // pass writes (P, dS) per entry in CSR order, and the column pass gathers them through the
   // CSC -> CSR entry map instead of recomputing q.k and dY.v per entry
   bool es = false;
   bool es_logits = false;          // the forward's logits are part of the state (GT_ES_LOGITS, default 1)
@@ -307,8 +307,8 @@ int launches_bwd(const gt_plan_s* P);
 
 // Materialised per-entry state of the ES kernels (all null: recompute kernels).
 struct EntryState {
-  float* out = nullptr;          // fwd: s2 [nnz_local][heads] | rowb: (P, dP) [nnz_local][heads][2]
-  const float* in = nullptr;     // rowb: s2 | colb: (P, dP)
+  float* out = nullptr;          // fwd: s2 [nnz_local][heads] | rowb: (P, dS) [nnz_local][heads] (bf16x2 | f32x2)
+  const float* in = nullptr;     // rowb: s2 | colb: (P, dS)
   const int32_t* src = nullptr;  // colb: entry -> local CSR entry (-1: remote row)
   // column pass over another entry list (the halo columns of the reduce-scatter backward)
   const int32_t* nbr = nullptr;  // neighbour (row) ids of the entries; null: the plan's CSC slice

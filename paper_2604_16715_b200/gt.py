@@ -313,7 +313,7 @@ class Plan:
     dtype "bf16" | "f32"; scale (0 -> 1 / sqrt(heads d)); world / rank / comm (LoopbackGroup or
     NcclComm) for multi-rank plans; strategy "auto" | "single" | "allgather" | "halo" | "a2a";
     heavy_threshold (0 -> 512); partition 0 (rows + edges) | 1 (nodes); edge_state 0 | 1 | -1
-    (materialised logits and (P, dP): auto / on / off); bwd_mode 0 (transposed owner) | 1
+    (materialised logits and (P, dS): auto / on / off); bwd_mode 0 (transposed owner) | 1
     (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); cuda_graphs (world-1 graph
     replay); beta_profile (JSON of measured beta per strategy for GT_AUTO instead of plan-time probes);
     profile (per-stage CUDA events); kv_fp8 (fp8 K||V storage, gt_opts.kv_fp8: world 1, bf16, entry state);
