@@ -18,11 +18,26 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KERNEL_SOURCES = ("paper_2604_16715_b200/csrc/attn_pipe.cu",)   # the three pass kernels
 
 
-def kernel_sha(root=ROOT):
+def code_of(text: str) -> str:
+    """The source without // comments and blank lines (comment edits do not change the kernels)."""
+    out = []
+    for line in text.splitlines():
+        i = line.find("//")
+        line = (line[:i] if i >= 0 else line).rstrip()
+        if line:
+            out.append(line)
+    return "\n".join(out)
+
+
+def kernel_sha(root=ROOT, texts=None):
     h = hashlib.sha256()
-    for f in KERNEL_SOURCES:
-        with open(os.path.join(root, f), "rb") as fh:
-            h.update(fh.read())
+    for i, f in enumerate(KERNEL_SOURCES):
+        if texts is not None:
+            t = texts[i]
+        else:
+            with open(os.path.join(root, f)) as fh:
+                t = fh.read()
+        h.update(code_of(t).encode())
     return h.hexdigest()[:16]
 
 
