@@ -29,6 +29,8 @@ CASES = {
     "peer_gather_allgather_w3": (("power", 2600, 32000, 75), (4, 64, "bf16"), 3, "allgather", 1, 0, -1),
     "a2a": (("power", 2200, 28000, 76), (4, 64, "bf16"), 2, "a2a", 0, 0, 1),
     "auto_communities": (("comm", 4096, 50000, 77), (8, 16, "f32"), 2, "auto", 0, 0, 1),
+    "halo_w4": (("power", 3000, 36000, 78), (4, 64, "bf16"), 4, "halo", 0, 0, 1),
+    "peer_gather_halo_w4": (("power", 3000, 36000, 79), (4, 64, "bf16"), 4, "halo", 1, 0, -1),
 }
 
 
@@ -122,3 +124,82 @@ def test_multiprocess_hostipc(case):
     assert len(names) == 1 and (strategy == "auto" or names == {strategy})
     for r in res:
         assert r[4]["transport"] == transport and r[4]["bwd_mode"] == bwd_mode
+
+
+# ---- distributed training across processes: the 3-layer graph transformer (Eq. 3-5) ----
+def _train_worker(rank, world, port, strategy, out_q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch
+        import torch.distributed as dist
+        import paper_2604_16715_b200 as gt
+        from tests.test_gpu_model import problem
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        rp, ci, X, params, labels, heads, scale = problem()
+        dim = X.shape[1]
+        grp = gt.HostIpcGroup()
+        plan = gt.Plan(rp, ci, heads, dim // heads, dtype="f32", scale=scale, world=world, rank=rank, comm=grp,
+                       strategy=strategy, heavy_threshold=64)
+        lo, hi = plan.row_lo, plan.row_hi
+        m = gt.GraphTransformer(params, heads)
+        x = torch.tensor(X[lo:hi], dtype=torch.float32).cuda()
+        lab = torch.tensor(labels[lo:hi], dtype=torch.int64).cuda()
+
+        def allreduce(ts):  # gradient and loss sums over ranks (gloo, host staging)
+            for t in ts:
+                c = t.detach().cpu()
+                dist.all_reduce(c)
+                t.copy_(c.to(t.device))
+
+        losses = [m.sgd_step(plan, x, lab, len(labels), 0.5, allreduce=allreduce) for _ in range(5)]
+        wc = m.wc.double().cpu().numpy()
+        plan.close()
+        grp.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        out_q.put((rank, (losses, wc), None))
+    except Exception:
+        out_q.put((rank, None, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("strategy", ["halo", "allgather"])
+def test_multiprocess_training_trajectory(strategy):
+    """Two processes (one rank each; attention exchange over CUDA IPC, gradient sums over gloo) train the
+    3-layer graph transformer for 5 SGD steps: the loss trajectory and final weights equal world 1's."""
+    import torch
+    import paper_2604_16715_b200 as gt
+    from tests._util import normwise
+    from tests.test_gpu_model import problem
+    rp, ci, X, params, labels, heads, scale = problem()
+    dim = X.shape[1]
+    plan1 = gt.Plan(rp, ci, heads, dim // heads, dtype="f32", scale=scale, heavy_threshold=64)
+    m1 = gt.GraphTransformer(params, heads)
+    tX = torch.tensor(X, dtype=torch.float32).cuda()
+    lab = torch.tensor(labels, dtype=torch.int64).cuda()
+    l1 = [m1.sgd_step(plan1, tX, lab, len(labels), 0.5) for _ in range(5)]
+    plan1.close()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, world, port, strategy, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res, errs = [None] * world, []
+    try:
+        for _ in range(world):
+            r, out, err = q.get(timeout=420)
+            if err:
+                errs.append((r, err))
+            res[r] = out
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+                p.join()
+    assert not errs, errs
+    for losses, wc in res:
+        assert max(abs(a - b) / abs(b) for a, b in zip(losses, l1)) <= 1e-4, (losses, l1)
+        assert normwise(wc, m1.wc.double().cpu().numpy()) <= 1e-4
