@@ -1508,15 +1508,15 @@ static gt_status fwd_bwd_host_streamed(gt_plan_t P, const void* q, const void* k
   cudaEvent_t* ev = P->e2e_cev.data();            // [0, C) q in, [C, 2C) dy in, [2C, 3C) fwd, [3C, 4C) row pass
   cudaEvent_t ev_start = P->e2e_ev[0], ev_kv = P->e2e_ev[1];
   const int C = P->e2e_c;
-  char* dq_ = (char*)P->h2d[0].p;
-  char* dk_ = (char*)P->h2d[1].p;
-  char* dv_ = (char*)P->h2d[2].p;
-  char* ddy = (char*)P->h2d[3].p;
-  char* dy_ = (char*)P->h2d[4].p;
-  float* dl = P->h2d[5].as<float>();
-  char* ddq = (char*)P->h2d[6].p;
-  char* ddk = (char*)P->h2d[7].p;
-  char* ddv = (char*)P->h2d[8].p;
+  char* q_d = (char*)P->h2d[0].p;
+  char* k_d = (char*)P->h2d[1].p;
+  char* v_d = (char*)P->h2d[2].p;
+  char* dy_d = (char*)P->h2d[3].p;
+  char* y_d = (char*)P->h2d[4].p;
+  float* lse_d = P->h2d[5].as<float>();
+  char* dq_d = (char*)P->h2d[6].p;
+  char* dk_d = (char*)P->h2d[7].p;
+  char* dv_d = (char*)P->h2d[8].p;
   auto h2d = [&](char* dst, const void* src, int64_t r0, int64_t r1, int64_t row) -> gt_status {
     if (r1 > r0)
       GT_CUDA_TRY(cudaMemcpyAsync(dst + r0 * row, (const char*)src + r0 * row, (size_t)((r1 - r0) * row),
@@ -1532,53 +1532,53 @@ static gt_status fwd_bwd_host_streamed(gt_plan_t P, const void* q, const void* k
   GT_CUDA_TRY(cudaEventRecord(ev_start, st));  // staging buffers are free once earlier work on `st` is done
   GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_in, ev_start, 0));
   GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev_start, 0));
-  GT_TRY(h2d(dk_, k, 0, P->n_local, rb));
-  GT_TRY(h2d(dv_, v, 0, P->n_local, rb));
+  GT_TRY(h2d(k_d, k, 0, P->n_local, rb));
+  GT_TRY(h2d(v_d, v, 0, P->n_local, rb));
   GT_CUDA_TRY(cudaEventRecord(ev_kv, P->e2e_in));
   for (int c = 0; c < Cr; ++c) {
-    GT_TRY(h2d(dq_, q, R[c], R[c + 1], rb));
+    GT_TRY(h2d(q_d, q, R[c], R[c + 1], rb));
     GT_CUDA_TRY(cudaEventRecord(ev[c], P->e2e_in));
   }
   for (int c = 0; c < Cr; ++c) {
-    GT_TRY(h2d(ddy, dy, R[c], R[c + 1], rb));
+    GT_TRY(h2d(dy_d, dy, R[c], R[c + 1], rb));
     GT_CUDA_TRY(cudaEventRecord(ev[C + c], P->e2e_in));
   }
   // forward, in row chunks
   GT_CUDA_TRY(cudaStreamWaitEvent(st, ev_kv, 0));
-  if (P->kv_fp8) GT_TRY(requantize(P, dk_, dv_, st));
-  if (P->n_hot) GT_TRY(repack_hot(P, dk_, dv_, st));
+  if (P->kv_fp8) GT_TRY(requantize(P, k_d, v_d, st));
+  if (P->n_hot) GT_TRY(repack_hot(P, k_d, v_d, st));
   for (int c = 0; c < Cr; ++c) {
     GT_CUDA_TRY(cudaStreamWaitEvent(st, ev[c], 0));
-    GT_TRY(launch_pass_range(P, 0, dq_, dk_, dv_, nullptr, dl, nullptr, dy_, nullptr, st, P->e2e_t[0][c],
+    GT_TRY(launch_pass_range(P, 0, q_d, k_d, v_d, nullptr, lse_d, nullptr, y_d, nullptr, st, P->e2e_t[0][c],
                              P->e2e_t[0][c + 1], P->e2e_h[0][c], P->e2e_h[0][c + 1], c == 0));
     GT_CUDA_TRY(cudaEventRecord(ev[2 * C + c], st));
   }
-  set_fwd_tag(P, dq_, dk_, dv_, dl);
+  set_fwd_tag(P, q_d, k_d, v_d, lse_d);
   // row pass, in row chunks
   for (int c = 0; c < Cr; ++c) {
     GT_CUDA_TRY(cudaStreamWaitEvent(st, ev[C + c], 0));
-    GT_TRY(launch_pass_range(P, 1, dq_, dk_, dv_, dy_, dl, ddy, ddq, nullptr, st, P->e2e_t[0][c], P->e2e_t[0][c + 1],
+    GT_TRY(launch_pass_range(P, 1, q_d, k_d, v_d, y_d, lse_d, dy_d, dq_d, nullptr, st, P->e2e_t[0][c], P->e2e_t[0][c + 1],
                              P->e2e_h[0][c], P->e2e_h[0][c + 1], c == 0));
     GT_CUDA_TRY(cudaEventRecord(ev[3 * C + c], st));
   }
   // outputs of the forward and the row pass leave while the column pass runs
   for (int c = 0; c < Cr; ++c) {
     GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev[2 * C + c], 0));
-    GT_TRY(d2h(y, dy_, R[c], R[c + 1], rb));
-    GT_TRY(d2h(lse, (const char*)dl, R[c], R[c + 1], lb));
+    GT_TRY(d2h(y, y_d, R[c], R[c + 1], rb));
+    GT_TRY(d2h(lse, (const char*)lse_d, R[c], R[c + 1], lb));
   }
   for (int c = 0; c < Cr; ++c) {
     GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev[3 * C + c], 0));
-    GT_TRY(d2h(dq, ddq, R[c], R[c + 1], rb));
+    GT_TRY(d2h(dq, dq_d, R[c], R[c + 1], rb));
   }
   // column pass, in column chunks (reusing the forward's events, whose waits are already enqueued)
   for (int c = 0; c < Cc; ++c) {
-    GT_TRY(launch_pass_range(P, 2, dq_, dk_, dv_, nullptr, nullptr, ddy, ddk, ddv, st, P->e2e_t[1][c],
+    GT_TRY(launch_pass_range(P, 2, q_d, k_d, v_d, nullptr, nullptr, dy_d, dk_d, dv_d, st, P->e2e_t[1][c],
                              P->e2e_t[1][c + 1], P->e2e_h[1][c], P->e2e_h[1][c + 1], c == 0));
     GT_CUDA_TRY(cudaEventRecord(ev[4 * C + (c & 3)], st));
     GT_CUDA_TRY(cudaStreamWaitEvent(P->e2e_out, ev[4 * C + (c & 3)], 0));
-    GT_TRY(d2h(dk, ddk, Rc[c], Rc[c + 1], rb));
-    GT_TRY(d2h(dv, ddv, Rc[c], Rc[c + 1], rb));
+    GT_TRY(d2h(dk, dk_d, Rc[c], Rc[c + 1], rb));
+    GT_TRY(d2h(dv, dv_d, Rc[c], Rc[c + 1], rb));
   }
   GT_CUDA_TRY(cudaStreamSynchronize(P->e2e_out));
   GT_CUDA_TRY(cudaStreamSynchronize(st));
