@@ -241,7 +241,7 @@ class Clocks:
         except Exception:
             self.proc.kill()
             return None
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -250,6 +250,7 @@ class Clocks:
             try:
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for nm, val in zip(names, f[5:9]):
@@ -258,7 +259,9 @@ class Clocks:
         if not sm:
             return None
         sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        pw.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": pw[len(pw) // 2] if pw else None, "power_w_max": pw[-1] if pw else None}
 
 
 def report_fields(per_step, stages, info, world, nnz, step_bytes, peak):
