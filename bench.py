@@ -121,7 +121,7 @@ def l2_peak():
         return None
 
 
-def physical_roofline(cfg, dom, stage_ms, per, units, comp, peak, peak_src):
+def physical_roofline(cfg, dom, stage_ms, per, units, comp, peak, peak_src, world=1):
     """The dominant pass against the HBM roofline, physically: DRAM bytes ncu measured for this kernel
     (per launch, cold cache, profiles/ncu_traffic.json) over its live CUDA-event launch time, as a
     fraction of the measured HBM peak; this cannot exceed 1 by construction.  Next
@@ -131,7 +131,9 @@ def physical_roofline(cfg, dom, stage_ms, per, units, comp, peak, peak_src):
     whose ncu utilisation is highest ("binding")."""
     t = stage_ms[dom] * 1e-3
     gather = per[dom][0] * units[dom][0] + per[dom][1] * units[dom][1]
-    rec, current = ncu_record(cfg.name, dom)
+    # the committed ncu counters are those of the world-1 kernels (one rank's launches cover the whole
+    # graph); at world > 1 a rank's launches cover its rows only, so only the models are reported
+    rec, current = ncu_record(cfg.name, dom) if world == 1 else (None, None)
     dram = rec["dram_bytes"] if rec else None
     out = {"bound": "hbm", "kernel": dom, "launch_ms": stage_ms[dom], "peak": peak, "unit": "GB/s",
            "peak_source": peak_src,
@@ -148,7 +150,7 @@ def physical_roofline(cfg, dom, stage_ms, per, units, comp, peak, peak_src):
            "all_passes": {}}
     l2p = l2_peak()
     for s_, ms_ in stage_ms.items():
-        r, _ = ncu_record(cfg.name, s_)
+        r, _ = ncu_record(cfg.name, s_) if world == 1 else (None, None)
         e = {"ms": ms_, "compulsory_frac": comp[s_] / (ms_ * 1e-3) / 1e9 / peak}
         if r:
             e["dram_frac"] = r["dram_bytes"] / (ms_ * 1e-3) / 1e9 / peak
@@ -176,7 +178,9 @@ def physical_roofline(cfg, dom, stage_ms, per, units, comp, peak, peak_src):
     return out
 
 
-def step_dram_frac(cfg, ms, peak):
+def step_dram_frac(cfg, ms, peak, world=1):
+    if world != 1:
+        return None
     tot = 0.0
     for s_ in ("fwd", "bwd_rows", "bwd_cols"):
         r, _ = ncu_record(cfg.name, s_)
@@ -498,7 +502,8 @@ def run_ours(args):
              "bwd_cols": (info["nnz_in_local"], info["n_local"])}
     peak, peak_src = peaks()
     step_bytes = sum(per[s][0] * units[s][0] + per[s][1] * units[s][1] for s in per)
-    roofline = physical_roofline(cfg, dom, stage_ms, per, units, compulsory_bytes(info, h, d, elt), peak, peak_src)
+    roofline = physical_roofline(cfg, dom, stage_ms, per, units, compulsory_bytes(info, h, d, elt), peak, peak_src,
+                                 world)
 
     # ---- end to end through the C ABI with pinned host buffers ----
     e2e = None
@@ -567,7 +572,7 @@ def run_ours(args):
             "roofline": roofline,
             # whole step: ncu DRAM bytes of the three passes over the step time (physical), and the
             # no-reuse gather model (exceeds 1 on L2-local graphs: a model, not a fraction of the peak)
-            "step_dram_frac": step_dram_frac(cfg, ms, peak),
+            "step_dram_frac": step_dram_frac(cfg, ms, peak, world),
             "step_gather_model_frac": (step_bytes / (ms * 1e-3) / 1e9) / peak,
             "stages_ms": {s: stages[s][0] / max(stages[s][1], 1) for s in stages},
             "cpu_baseline": cpu, "e2e": e2e,
