@@ -48,6 +48,9 @@ def parse():
                     help="gt_opts.kv_fp8: fp8 K||V storage (NEXT-4 option; not the bf16 headline)")
     ap.add_argument("--hot-cols", type=int, default=int(os.environ.get("GT_HOT_COLS", "0")),
                     help="gt_opts.hot_cols: hot-column K||V table in persisting L2 (world 1)")
+    ap.add_argument("--comm", choices=["nccl", "hostipc"], default="nccl",
+                    help="world > 1 transport: NCCL (one GPU per process) or CUDA IPC bootstrapped over gloo "
+                         "(several processes may share a GPU: a functional check of the multi-rank path)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -415,14 +418,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    if args.comm == "hostipc":  # processes may share a device
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and args.comm == "nccl":
         # NCCL's communicator lines (rank, nranks, device, transport) go to stderr so the driver can check
         # the ranks; stdout keeps the one JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif world > 1:
+        dist.init_process_group("gloo")
     if rank == 0:
         _build.build()
     if world > 1:
@@ -437,7 +444,7 @@ def run_ours(args):
     n, nnz = len(rp) - 1, len(ci)
     t_gen = time.perf_counter() - t_gen
 
-    comm = gt.NcclComm() if world > 1 else None
+    comm = (gt.NcclComm() if args.comm == "nccl" else gt.HostIpcGroup()) if world > 1 else None
     strategy = args.strategy or ("single" if world == 1 else "auto")
     t_plan = time.perf_counter()
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
@@ -490,7 +497,7 @@ def run_ours(args):
     stages = plan.timings()
     clk = clocks.stop() if rank == 0 else None
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=q.device)
+        t = torch.tensor([ms], dtype=torch.float64, device=q.device if args.comm == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
@@ -519,7 +526,7 @@ def run_ours(args):
             plan.fwd_bwd_host(pin["q"], pin["k"], pin["v"], pin["dy"], outs[0], plse, outs[1], outs[2], outs[3])
         te = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
-            t = torch.tensor([te], dtype=torch.float64, device=q.device)
+            t = torch.tensor([te], dtype=torch.float64, device=q.device if args.comm == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         tb = (hi - lo) * h * d * elt
@@ -562,6 +569,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": cfg.name, "nodes": n, "nnz": nnz, "heads": h, "head_dim": d,
                        "strategy": info["strategy_name"], "parallelism": f"graph-row x{world}",
+                       "comm": args.comm if world > 1 else None,
                        "l2": f"inputs larger than L2 (K, V tables {n * h * d * elt / 1e9:.2f} GB each vs 126 MB L2); "
                              "no flush",
                        "edges_per_s_per_gpu": value / world, "heavy_threshold": args.heavy or 512,
