@@ -136,6 +136,25 @@ def test_fp8_degenerate(case):
     plan.close()
 
 
+def test_fp8_bitwise_deterministic():
+    """No atomics in the numerics: two fp8 steps on the same inputs are bitwise identical."""
+    import torch
+    import paper_2604_16715_b200 as gt
+    rp, ci = gtgen.random_graph(2500, 40000, seed=91, directed=True, power=2.0)
+    n, h, d = len(rp) - 1, 4, 64
+    ins = [to_torch(x) for x in inputs(n, h, d, "bf16", 911)]
+    plan = gt.Plan(rp, ci, h, d, dtype="bf16", heavy_threshold=48, kv_fp8=True)
+    outs = []
+    for _ in range(2):
+        y, lse = plan.fwd(*ins[:3])
+        g = plan.bwd(*ins[:3], y, lse, ins[3])
+        torch.cuda.synchronize()
+        outs.append([t.clone() for t in (y, lse, *g)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    plan.close()
+
+
 def test_fp8_config_errors():
     import paper_2604_16715_b200 as gt
     rp, ci = gtgen.random_graph(300, 2000, seed=5, power=2.3)

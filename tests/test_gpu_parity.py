@@ -187,12 +187,21 @@ def test_host_buffer_streamed_chunks(gt, chunks, monkeypatch):
         assert normwise(to_f64(y), Y) <= 2e-2 and normwise(to_f64(dq), DQ) <= 2e-2
         assert normwise(to_f64(dk), DK) <= 2e-2 and normwise(to_f64(dv), DV) <= 2e-2
         check_lse(lse.numpy(), LSE, "bf16")
+    # bitwise reproducible across calls (the chunk schedule does not change the arithmetic order)
+    outs2 = [torch.empty_like(tq).pin_memory() for _ in range(4)]
+    lse2 = torch.empty((n, h), dtype=torch.float32).pin_memory()
+    plan.fwd_bwd_host(tq, tk, tv, tdy, outs2[0], lse2, outs2[1], outs2[2], outs2[3])
+    for a, b in zip((y, dq, dk, dv, lse), (*outs2, lse2)):
+        assert torch.equal(a, b)
     # the device API afterwards sees a consistent plan (the host path left the forward state tagged)
     dev = [to_torch(x) for x in (q, k, v, dy)]
     yd, ld = plan.fwd(*dev[:3])
     g = plan.bwd(*dev[:3], yd, ld, dev[3])
     torch.cuda.synchronize()
     assert normwise(to_f64(g[0]), DQ) <= 2e-2 and normwise(to_f64(g[1]), DK) <= 2e-2
+    # and the chunked host schedule computes exactly what the device API computes
+    for a, b in zip((yd, ld, *g), (y, lse, dq, dk, dv)):
+        assert torch.equal(a.cpu(), b)
     plan.close()
 
 
