@@ -46,6 +46,8 @@ def parse():
                     help="gt_opts.bwd_mode (world > 1): 0 transposed owner, 1 reduce-scatter of fp32 partials")
     ap.add_argument("--kv-fp8", type=int, default=int(os.environ.get("GT_KV_FP8", "0")),
                     help="gt_opts.kv_fp8: fp8 K||V storage (NEXT-4 option; not the bf16 headline)")
+    ap.add_argument("--reserve-sms", type=int, default=int(os.environ.get("GT_RESERVE_SMS", "0")),
+                    help="gt_opts.reserve_sms (world > 1): SMs left to NCCL during the forward overlap (0 -> 16)")
     ap.add_argument("--hot-cols", type=int, default=int(os.environ.get("GT_HOT_COLS", "0")),
                     help="gt_opts.hot_cols: hot-column K||V table in persisting L2 (world 1)")
     ap.add_argument("--comm", choices=["nccl", "hostipc"], default="nccl",
@@ -450,7 +452,8 @@ def run_ours(args):
     plan = gt.Plan(rp, ci, h, d, dtype=cfg.dtype, scale=scale, world=world, rank=rank, comm=comm,
                    strategy=strategy, heavy_threshold=args.heavy, profile=True, device=local,
                    edge_state=args.edge_state, bwd_mode=args.bwd_mode, transport=args.transport,
-                   kv_fp8=bool(args.kv_fp8), hot_cols=args.hot_cols if world == 1 else 0)
+                   kv_fp8=bool(args.kv_fp8), hot_cols=args.hot_cols if world == 1 else 0,
+                   reserve_sms=args.reserve_sms)
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan
     info = plan.info()

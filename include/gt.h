@@ -164,6 +164,9 @@ typedef struct {
                               not the last forward's re-quantises them.  Needs world == 1, a bf16
                               plan, heads * d >= 128 and the materialised entry state (edge_state
                               >= 0 and fitting); else GT_ECONFIG.  0 => K, V gathered as given. */
+  int reserve_sms;         /* world > 1: SMs per GPU left free for the communication kernels while the
+                              forward's owned-column phase overlaps the K || V exchange; 0 => 16, -1 =>
+                              none (tune per interconnect / NCCL channel count) */
   int hot_cols;            /* > 0 => hot-column table (world 1; not with kv_fp8): the K || V rows of the
                               hot_cols columns with the most entries (power-law hubs, e.g. R-MAT) are
                               packed by every gt_attn_fwd into one contiguous plan table that the

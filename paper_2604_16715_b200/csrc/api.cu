@@ -499,6 +499,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   if (!(opts->scale >= 0.f) || std::isinf(opts->scale)) return fail(GT_EINVAL, "gt_plan: bad scale");
   if (opts->kv_fp8 != 0 && opts->kv_fp8 != 1) return fail(GT_EINVAL, "gt_plan: kv_fp8 must be 0 or 1");
   if (opts->hot_cols < 0) return fail(GT_EINVAL, "gt_plan: hot_cols must be >= 0");
+  if (opts->reserve_sms < -1) return fail(GT_EINVAL, "gt_plan: reserve_sms must be >= -1");
   if (opts->hot_cols > 0 && (world != 1 || opts->kv_fp8))
     return fail(GT_ECONFIG, "gt_plan: hot_cols needs world == 1 and kv_fp8 == 0");
   if (opts->kv_fp8 && (world != 1 || opts->dtype != GT_BF16 || (int64_t)heads * d < 128 || opts->edge_state < 0))
@@ -520,6 +521,7 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
   P->nnz = nnz;
   P->scale = opts->scale > 0.f ? opts->scale : (float)(1.0 / std::sqrt((double)heads * d));
   P->heavy_threshold = opts->heavy_threshold > 0 ? opts->heavy_threshold : 512;  // A/B-tuned on C3
+  P->reserve_sms = opts->reserve_sms == 0 ? 16 : (opts->reserve_sms < 0 ? 0 : opts->reserve_sms);
   P->profile = opts->profile != 0;
   P->bwd_reduce = world > 1 && opts->bwd_mode == 1;
   P->graphs = opts->cuda_graphs != 0;

@@ -25,7 +25,6 @@ namespace {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr int kBlock = 256;
-constexpr int kReserveSms = 16;   // SMs left to NCCL kernels while the forward halo is in flight
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -340,7 +339,7 @@ gt_status launch_fwd(gt_plan_s* P, const void* q, const void* k, const void* v, 
                      entry_state(P, 0)));
   } else {
     GT_TRY(pipe_pass(P, 0, P->w_fwd[0], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st,
-                     kReserveSms, entry_state(P, 0)));
+                     P->reserve_sms, entry_state(P, 0)));
     if (halo_ready) GT_CUDA_TRY(cudaStreamWaitEvent(st, halo_ready, 0));
     GT_TRY(pipe_pass(P, 0, P->w_fwd[1], ct, part, q, nullptr, nullptr, k, v, halo_kv, nullptr, y, nullptr, lse, st, 0,
                      entry_state(P, 0)));

@@ -265,6 +265,7 @@ struct gt_plan_s {
   gt::DevBuf d_kv8, d_kvref;
   int64_t kv8_row = 0;
   const void* kv8_tag[2] = {nullptr, nullptr};
+  int reserve_sms = 16;            // gt_opts.reserve_sms: SMs left to NCCL during the forward's overlap
   // hot-column table (gt_opts.hot_cols, world 1): packed [k | v] rows of the top in-degree columns
   int64_t n_hot = 0, hot_entries = 0;
   gt::DevBuf d_hot, d_hot_idx;

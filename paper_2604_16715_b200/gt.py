@@ -41,7 +41,8 @@ class _Opts(ctypes.Structure):
                 ("validate", ctypes.c_int), ("partition", ctypes.c_int), ("device", ctypes.c_int),
                 ("heavy_threshold", ctypes.c_int), ("beta_profile", ctypes.c_char_p), ("profile", ctypes.c_int),
                 ("edge_state", ctypes.c_int), ("bwd_mode", ctypes.c_int), ("transport", ctypes.c_int),
-                ("cuda_graphs", ctypes.c_int), ("kv_fp8", ctypes.c_int), ("hot_cols", ctypes.c_int)]
+                ("cuda_graphs", ctypes.c_int), ("kv_fp8", ctypes.c_int), ("reserve_sms", ctypes.c_int),
+                ("hot_cols", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -317,14 +318,15 @@ class Plan:
     (reduce-scatter); transport 0 (copies) | 1 (fused peer gather); cuda_graphs (world-1 graph
     replay); beta_profile (JSON of measured beta per strategy for GT_AUTO instead of plan-time probes);
     profile (per-stage CUDA events); kv_fp8 (fp8 K||V storage, gt_opts.kv_fp8: world 1, bf16, entry state);
-    hot_cols (hot-column K||V table under a persisting L2 window, gt_opts.hot_cols: world 1).
+    hot_cols (hot-column K||V table under a persisting L2 window, gt_opts.hot_cols: world 1); reserve_sms
+    (world > 1: SMs left to the communication kernels during the forward's overlap; 0 -> 16, -1 -> none).
     """
 
     def __init__(self, row_ptr, col_idx, heads: int, d: int, dtype="bf16", scale: float = 0.0, world: int = 1,
                  rank: int = 0, comm=None, strategy="auto", heavy_threshold: int = 0, partition: int = 0,
                  validate: bool = True, device: int = -1, profile: bool = False, edge_state: int = 0,
                  bwd_mode: int = 0, transport: int = 0, cuda_graphs: bool = False, beta_profile=None,
-                 kv_fp8: bool = False, hot_cols: int = 0):
+                 kv_fp8: bool = False, hot_cols: int = 0, reserve_sms: int = 0):
         L = lib()
         self.row_ptr = np.ascontiguousarray(row_ptr, np.int64)
         self.col_idx = np.ascontiguousarray(col_idx, np.int32)
@@ -347,6 +349,7 @@ class Plan:
         opts.cuda_graphs = int(cuda_graphs)
         opts.kv_fp8 = int(kv_fp8)
         opts.hot_cols = int(hot_cols)
+        opts.reserve_sms = int(reserve_sms)
         self._beta_profile = str(beta_profile).encode() if beta_profile else None  # kept alive for gt_plan
         opts.beta_profile = self._beta_profile
         if world > 1:

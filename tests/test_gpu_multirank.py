@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=0, edge_state=0, bwd_mode=0,
-                 transport=0, steps=1, beta_profile=None):
+                 transport=0, steps=1, beta_profile=None, reserve_sms=0):
     import torch
     import paper_2604_16715_b200 as gt
     n = len(rp) - 1
@@ -36,7 +36,8 @@ def run_loopback(rp, ci, h, d, dtype, world, strategy, seed, heavy=0, partition=
             s = torch.cuda.Stream()
             plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, world=world, rank=r, comm=grp,
                            strategy=strategy, heavy_threshold=heavy, partition=partition, edge_state=edge_state,
-                           bwd_mode=bwd_mode, transport=transport, beta_profile=beta_profile)
+                           bwd_mode=bwd_mode, transport=transport, beta_profile=beta_profile,
+                           reserve_sms=reserve_sms)
             lo, hi = plan.row_lo, plan.row_hi
             with torch.cuda.stream(s):
                 tq, tk, tv, tdy = (t[lo:hi].contiguous() for t in full)
@@ -213,3 +214,11 @@ def test_auto_follows_a_beta_profile(tmp_path):
         assert {r[4]["strategy_name"] for r in res} == {fast}
         for r in res:
             assert r[4]["beta_s_per_row"][{"allgather": 2, "halo": 3}[fast]] == pytest.approx(1e-12)
+
+
+@pytest.mark.parametrize("reserve_sms", [-1, 40])
+def test_loopback_reserve_sms(reserve_sms):
+    """gt_opts.reserve_sms only changes how many SMs the overlapped phase leaves free, not the results."""
+    rp, ci = gtgen.random_graph(2500, 30000, seed=171, directed=True, power=2.1)
+    ins, res = run_loopback(rp, ci, 4, 64, "bf16", 2, "halo", seed=1710, heavy=64, reserve_sms=reserve_sms)
+    check(rp, ci, "bf16", ins, res, 2)
