@@ -70,6 +70,9 @@ constexpr int kMaxDevices = 64;
 #ifndef GT_PIPE_TMA
 #define GT_PIPE_TMA 0  // measured slower on C3; kept for A/B builds
 #endif
+#ifndef GT_PIPE_MMA
+#define GT_PIPE_MMA 0  // tensor-core (mma.sync) consumer for the products shape, bit p = pass p (measured slower: DESIGN.md section 6)
+#endif
 constexpr int kWarps = GT_PIPE_WARPS;   // warps per CTA
 #ifndef GT_COLB_STAGES
 #define GT_COLB_STAGES 2
@@ -176,7 +179,6 @@ struct PC {
   static constexpr int PDB = sizeof(T) == 2 ? 4 : 8;      // stored (P, dS) of one entry and head: bf16x2 | f32x2
   // the recompute column pass gathers each in-neighbour's (LSE2, D) block; with stored (P, dS) it does not
   static constexpr bool STATS = PASS == 2 && !(ES & 1);
-  static constexpr int EB = F8 ? GR : 2 * RB + (STATS ? SB : 0);                     // bytes per neighbour
   // own slot: fwd q | rowb [q] dY Y lse | colb [k v]   (the row pass recomputing q.k needs q; with
   // stored (P, dS) the column pass needs no own-column data)
   static constexpr int OWN_DY = PASS == 1 ? ((ES & 2) ? 0 : RB) : 0;
@@ -197,10 +199,19 @@ struct PC {
   // for the two feature rows of every neighbour when the stage holds exactly 4 neighbours; the
   // stage then keeps the 4 first rows (k | q) contiguous, then the 4 second rows (v | dY), then stats
   static constexpr bool TMA = GT_PIPE_TMA && U == 4 && !F8;
+  // Tensor-core consumer (Mma below): the stage's dot products and SpMM updates as mma.sync m16n8k16
+  // products for the products shape (bf16, 4 heads of 64, 4 neighbours per stage) - the forward, the
+  // row pass reading the forward's logits and the column pass reading the stored (P, dS)
+  static constexpr bool MMA = ((GT_PIPE_MMA >> PASS) & 1) && sizeof(T) == 2 && H == 4 && D == 256 && U == 4 && !F8 && !TMA &&
+                              (PASS == 0 || (PASS == 1 && (ES & 2)) || (PASS == 2 && (ES & 1)));
+  // bytes per neighbour in a stage; the tensor-core layout pads it to 32 mod 128 so that the 8 rows one
+  // ldmatrix phase reads (4 neighbours x 2 heads) fall in 8 distinct 16-byte bank groups
+  static constexpr int EB = (F8 ? GR : 2 * RB + (STATS ? SB : 0)) + (MMA ? 32 : 0);
   static constexpr int STAGE = (U * EB + AUX + 127) / 128 * 128;   // 128-byte aligned TMA destinations
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
   // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dS)[U][H]
-  static constexpr int XS = PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0);
+  // (the tensor-core consumer stores them from the registers of the lanes holding them: no scratch)
+  static constexpr int XS = MMA ? 0 : (PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0));
   static constexpr int kS = stages_of<PASS, ES>();                   // stages per warp
   static constexpr int MB = TMA ? kS * 8 : 0;                       // one mbarrier per stage
   static constexpr int WARP_SMEM = (kS * (STAGE + OWNP + XS) + MB + 127) / 128 * 128;
@@ -616,6 +627,144 @@ struct Bfly {
   }
 };
 
+// ---- tensor-core consumer: mma.sync m16n8k16 (bf16 operands, exact products, fp32 accumulation) ----
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t bf16x2_of(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void st_pred_bf16(char* p, float x, bool on) {
+  asm volatile("{.reg .pred q;\n\t.reg .b16 h;\n\tsetp.ne.b32 q, %2, 0;\n\tcvt.rn.bf16.f32 h, %1;\n\t"
+               "@q st.global.b16 [%0], h;}" ::"l"(p), "f"(x), "r"((int)on) : "memory");
+}
+
+// Lane geometry of the tensor-core consumer (H = 4 heads of 64 elements, U = 4 neighbours per stage,
+// lane = 4 g + t).
+//  * Dot products (q.k in the forward, dY.v in the row pass): per 16-element chunk c of the heads one
+//    m16n8k16 product D = A B with A[m = 4h + u][k] = neighbour u's head-h chunk c (ldmatrix of the
+//    staged rows; the two 8-element halves swapped for odd h, which puts the 8 rows of an ldmatrix
+//    phase in 8 bank groups given the 32-mod-128 neighbour stride) and B[k][n = h] = the own row's
+//    head h in the same element order (registers, once per row; B[.][n >= 4] = 0).  Only the diagonal
+//    D[4h + u][h] is used: lane 4g + t, t < 2 ("holder"), ends with entry (h = 2t + g/4, u = g % 4).
+//  * SpMM (y += p v, dQ += dS k, dV += P dY, dK += dS q): the transposed product D'[i][n] +=
+//    A'[i][k] B'[k][n] with A'[i][4h + u] = neighbour u's head-h element tau_h(c, i) (ldmatrix.trans)
+//    and B'[4h + u][n] = w(u, h) for n = h, else 0 (block diagonal: 2 registers from 4 shuffles).
+//    Holder lane 4g + t accumulates heads 2t, 2t + 1: acc[c] = {y_2t[16c + g], y_2t+1[16c + 8 + g],
+//    y_2t[16c + 8 + g], y_2t+1[16c + g]}.
+//  Products are exact (bf16 x bf16) and summed in fp32, as in the FHFMA.BF16 consumer; the weights
+//  p, dS, P are rounded to bf16 first, as there.
+struct Mma {
+  int g, t;
+  bool holder;             // t < 2: holds one (head, neighbour) product
+  int h, u;                // holder: its entry's head and neighbour
+  int src_e;               // lane holding the product of entry-state slot `lane` = 4 u' + h' (u' < 4)
+  bool b0on, b1on;         // B' registers this lane supplies (heads t/2 and 2 + t/2)
+  uint32_t off_dot, off_sp;  // byte offsets (within a stage's first row block) of the ldmatrix rows
+  template <int EB>
+  __device__ __forceinline__ void init(int lane) {
+    g = lane >> 2;
+    t = lane & 3;
+    holder = t < 2;
+    h = (2 * t + (g >> 2)) & 3;
+    u = g & 3;
+    const int eh = lane & 3, eu = (lane >> 2) & 3;
+    src_e = 16 * (eh & 1) + 4 * eu + (eh >> 1);
+    b0on = g == (t >> 1);
+    b1on = g == 2 + (t >> 1);
+    const int j = lane >> 3, r = lane & 7;
+    const int hd = 2 * (j & 1) + (r >> 2), hs = 2 * (j >> 1) + (r >> 2);
+    off_dot = (uint32_t)((r & 3) * EB + hd * 128 + 16 * (((j >> 1) + hd) & 1));
+    off_sp = (uint32_t)((r & 3) * EB + hs * 128 + 16 * (((j & 1) + hs) & 1));
+  }
+  // B fragments of the own row (512-byte bf16 row at shared address `o`): b[2c], b[2c + 1]
+  __device__ __forceinline__ void load_b(const char* o, uint32_t (&b)[8]) const {
+    const int gg = g & 3;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(o);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int e0 = gg * 64 + 16 * c + 8 * (gg & 1) + 2 * t, e1 = gg * 64 + 16 * c + 8 * ((gg + 1) & 1) + 2 * t;
+      b[2 * c] = g < 4 ? w[e0 >> 1] : 0u;
+      b[2 * c + 1] = g < 4 ? w[e1 >> 1] : 0u;
+    }
+  }
+  // the 16 dot products of a stage (rows at shared address `rows` + off_dot); holder lanes' value is theirs
+  __device__ __forceinline__ float dot(uint32_t rows, const uint32_t (&b)[8]) const {
+    float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t a0[4], a1[4];
+    ldsm4(rows, a0);
+    ldsm4(rows + 32, a1);
+    mma16816(d0, a0, b[0], b[1]);
+    mma16816(d1, a1, b[2], b[3]);
+    ldsm4(rows + 64, a0);
+    ldsm4(rows + 96, a1);
+    mma16816(d0, a0, b[4], b[5]);
+    mma16816(d1, a1, b[6], b[7]);
+    const bool lo = g < 4, odd = t & 1;
+    const float x0 = odd ? (lo ? d0[2] : d0[3]) : (lo ? d0[0] : d0[1]);
+    const float x1 = odd ? (lo ? d1[2] : d1[3]) : (lo ? d1[0] : d1[1]);
+    return x0 + x1;
+  }
+  // B' registers of the weights w held by the holder lanes (rounded to bf16)
+  __device__ __forceinline__ void weights(float w, int lane, uint32_t& b0, uint32_t& b1) const {
+    const float wn = __shfl_sync(kFull, w, (lane + 4) & 31);   // neighbour u + 1 of the same head
+    const uint32_t pair = bf16x2_of(w, wn);
+    const uint32_t w0 = __shfl_sync(kFull, pair, 8 * t), w1 = __shfl_sync(kFull, pair, 8 * t + 1);
+    b0 = b0on ? w0 : 0u;
+    b1 = b1on ? w1 : 0u;
+  }
+  // acc[c] += A'(rows at shared address `rows` + off_sp) B'
+  __device__ __forceinline__ void spmm(uint32_t rows, uint32_t b0, uint32_t b1, float (&acc)[4][4]) const {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t a[4];
+      ldsm4t(rows + 32 * c, a);
+      mma16816(acc[c], a, b0, b1);
+    }
+  }
+  // element index (within a 256-element row) of acc[c][i]
+  __device__ __forceinline__ int elem(int c, int i) const {
+    const int hh = 2 * t + (i & 1);
+    return hh * 64 + 16 * c + ((i == 1 || i == 2) ? 8 : 0) + g;
+  }
+  __device__ __forceinline__ void store_bf16(char* row, const float (&acc)[4][4], float fe, float fo) const {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) st_pred_bf16(row + 2 * elem(c, i), acc[c][i] * ((i & 1) ? fo : fe), holder);
+  }
+  __device__ __forceinline__ void store_f32(float* row, const float (&acc)[4][4]) const {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) st_pred(row + elem(c, i), acc[c][i], holder);
+  }
+  __device__ __forceinline__ void scale(float (&acc)[4][4], float fe, float fo) const {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc[c][0] *= fe;
+      acc[c][1] *= fo;
+      acc[c][2] *= fe;
+      acc[c][3] *= fo;
+    }
+  }
+};
+constexpr float kRescale = 8.f;  // forward (tensor-core consumer): the running reference max of a head is
+                                 // raised only when a score exceeds it by more than 2^8 (weights <= 256)
+
 struct Meta {      // warp-uniform description of one filled stage
   int32_t e0;      // entry index (in `nbr` order) of the stage's first neighbour (nnz < 2^31)
   int32_t own;     // row/column id, or chunk -1 - c
@@ -638,13 +787,21 @@ struct Meta {      // warp-uniform description of one filled stage
 #ifndef GT_CARVEOUT  // preferred shared-memory carveout (percent of the unified L1/shared array); -1 = driver's
 #define GT_CARVEOUT 100
 #endif
-template <int PASS, int ES, int EPL>
+#ifndef GT_MMA_BWD_MINB  // tensor-core backward passes: resident CTAs per SM (register cap)
+#define GT_MMA_BWD_MINB 5
+#endif
+template <typename T, int H, int D, int PASS, int ES>
 constexpr int min_ctas() {
-  return EPL > 8 ? 1 : ((ES & 4) ? 5 : (PASS == 1 ? GT_ROWB_MINB : (PASS == 2 ? GT_COLB_MINB : GT_FWD_MINB)));
+  constexpr int EPL = D / 32;
+  return EPL > 8 ? 1
+                 : ((ES & 4) ? 5
+                             : (PASS == 0 ? GT_FWD_MINB
+                                          : (PC<T, H, D, PASS, ES>::MMA ? GT_MMA_BWD_MINB
+                                                                       : (PASS == 1 ? GT_ROWB_MINB : GT_COLB_MINB))));
 }
 
 template <typename T, int H, int D, int PASS, bool HALO, int ES>
-__global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
+__global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
     pipe_kernel(const PArgs a, const __grid_constant__ TmaMaps tm) {
   static_assert(!((ES & 1) && PASS == 2 && HALO), "the ES column pass reads local rows only");
   using C = PC<T, H, D, PASS, ES>;
@@ -920,6 +1077,13 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
   float fo = 1.f, ifo = 1.f, fq = 1.f;
   const float rk = C::F8 ? exp2i(__ldg(a.kvref)) : 1.f, rv = C::F8 ? exp2i(__ldg(a.kvref + 1)) : 1.f;
   const float irk = 1.f / rk, irv = 1.f / rv;
+  // tensor-core consumer: lane geometry, own-row B fragments, accumulators (Mma)
+  Mma mg;
+  if constexpr (C::MMA) mg.init<EB>(lane);
+  uint32_t bq[C::MMA ? 8 : 1];
+  float macc[C::MMA ? 4 : 1][4], macc2[(C::MMA && PASS == 2) ? 4 : 1][4];
+  float mh = 0.f, dh = 0.f;   // row pass: the holder's (LSE2, D) of its head
+  const uint32_t st_sh = su32(stages);
 
   Meta md[kS];
 #pragma unroll
@@ -931,7 +1095,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
       cp_wait<kS - 1>();
-      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8) __syncwarp();  // blocks copied by other lanes
+      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8 || C::MMA) __syncwarp();  // blocks copied by other lanes
       const Meta cur = md[s];
       if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one (no copy in flight)
       if constexpr (kTma) {
@@ -941,7 +1105,33 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
       const char* st = stages + s * C::STAGE;
       if (cur.first) {
         const char* o = owns + s * C::OWNP;
-        if constexpr (PASS == 0) {
+        if constexpr (C::MMA) {
+          if constexpr (PASS == 0) {
+            mg.load_b(o, bq);   // q
+            m = -INFINITY;      // per holder lane: its head's reference max; l its entry group's sum
+            l = 0.f;
+          } else if constexpr (PASS == 1) {
+            lds_raw<W>(o + C::OWN_DY + lane * LB, ow);
+            uint32_t yw[W];
+            lds_raw<W>(o + C::OWN_Y + lane * LB, yw);
+            // D_i = <dY_i, Y_i> (Sum_e P_e = 1); (m, l) = (LSE2, D) of head lane / LPH
+            l = head_sum<LPH>(dot_raw<T, W>(ow, yw));
+            m = reinterpret_cast<const float*>(o + C::OWN_LSE)[lane] * kLog2e;
+            mh = __shfl_sync(kFull, m, LPH * mg.h);
+            dh = __shfl_sync(kFull, l, LPH * mg.h);
+            mg.load_b(o + C::OWN_DY, bq);   // dY
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) macc[c][i] = 0.f;
+          if constexpr (PASS == 2) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) macc2[(PASS == 2) ? c : 0][i] = 0.f;
+          }
+        } else if constexpr (PASS == 0) {
           lds_raw<W>(o + lane * LB, ow);
           if constexpr (C::F8) fo = a.qscale * exp2i(to_f16_norm<EPL, LPH>(ow, oh));
 #pragma unroll
@@ -974,7 +1164,57 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
         }
       }
       const int cnt = cur.cnt;
-      if constexpr (C::F8 && PASS == 0) {
+      if constexpr (C::MMA && PASS == 0) {
+        // Forward on the tensor cores (Mma): s = qscale <q_i, k_j> for the stage's 16 (head, neighbour)
+        // pairs, base-2 online softmax against a per-head reference max m (raised only when a score
+        // exceeds it by 2^kRescale: the warp-uniform rescale is rare), y += p v
+        const uint32_t sa = st_sh + s * C::STAGE;
+        const float sv = mg.dot(sa + mg.off_dot, bq) * a.qscale;
+        const float sl = mg.holder ? (mg.u < cnt ? sv : -INFINITY) : 0.f;
+        if constexpr (ES & 2)  // s2[entry e0 + u][head] for the row pass: one coalesced store per stage
+          st_pred(a.es_out + (int64_t)cur.e0 * H + lane, __shfl_sync(kFull, sv, mg.src_e), lane < cnt * H);
+        float smax = fmaxf(sl, __shfl_xor_sync(kFull, sl, 4));
+        smax = fmaxf(smax, __shfl_xor_sync(kFull, smax, 8));
+        const bool grow = smax > m + kRescale;
+        if (__any_sync(kFull, grow)) {
+          const float mn = grow ? smax : m;
+          const float corr = ex2(m - mn);
+          l *= corr;
+          mg.scale(macc, __shfl_sync(kFull, corr, mg.t), __shfl_sync(kFull, corr, 16 + mg.t));
+          m = mn;
+        }
+        const float p = ex2(sl - m);   // 0 for masked neighbours
+        l += p;
+        uint32_t b0, b1;
+        mg.weights(p, lane, b0, b1);
+        mg.spmm(sa + RB + mg.off_sp, b0, b1, macc);
+      } else if constexpr (C::MMA && PASS == 1) {
+        // Row pass on the tensor cores: dP = <dY_i, v_j>, p = 2^(s2 - LSE2_i) from the forward's logit,
+        // dS = p (dP - D_i), (p, dS) stored per entry, dQ += dS k_j
+        const uint32_t sa = st_sh + s * C::STAGE;
+        const float dp = mg.dot(sa + RB + mg.off_dot, bq);
+        const float s_ = reinterpret_cast<const float*>(st + U * EB)[mg.u * H + mg.h];
+        const float p = mg.u < cnt ? ex2(s_ - mh) : 0.f;
+        const float ds = p * (dp - dh);
+        if constexpr (ES & 1)
+          st_pred_u32(reinterpret_cast<uint32_t*>(a.es_out) + (int64_t)cur.e0 * H + lane,
+                      __shfl_sync(kFull, pack_pd_bf16(p, ds), mg.src_e), lane < cnt * H);
+        uint32_t b0, b1;
+        mg.weights(ds, lane, b0, b1);
+        mg.spmm(sa + mg.off_sp, b0, b1, macc);
+      } else if constexpr (C::MMA && PASS == 2) {
+        // Column pass on the tensor cores: dV_j += P dY_i, dK_j += dS q_i with the row pass's (P, dS)
+        // (bf16x2 {lo P, hi dS}; zero-filled for masked neighbours) as block-diagonal B' registers
+        const uint32_t sa = st_sh + s * C::STAGE;
+        const uint32_t* aux = reinterpret_cast<const uint32_t*>(st + U * EB);
+        const int hb = mg.t >> 1, u0 = 2 * (mg.t & 1);
+        const uint32_t wa = aux[u0 * H + hb], wb = aux[(u0 + 1) * H + hb];
+        const uint32_t wc = aux[u0 * H + hb + 2], wd = aux[(u0 + 1) * H + hb + 2];
+        const uint32_t p0 = mg.b0on ? __byte_perm(wa, wb, 0x5410) : 0u, p1 = mg.b1on ? __byte_perm(wc, wd, 0x5410) : 0u;
+        const uint32_t d0 = mg.b0on ? __byte_perm(wa, wb, 0x7632) : 0u, d1 = mg.b1on ? __byte_perm(wc, wd, 0x7632) : 0u;
+        mg.spmm(sa + RB + mg.off_sp, p0, p1, macc2);
+        mg.spmm(sa + mg.off_sp, d0, d1, macc);
+      } else if constexpr (C::F8 && PASS == 0) {
         // fp8 forward: s = qscale 2^eq 2^ek_j <q', k8_j>, p~ = 2^(s - m), acc += f16(p~ 2^(ev_j - E_v)) v8_j
         // (y = acc 2^E_v / l); the dots are reduce-scattered by the butterfly as in the bf16 path, in
         // groups of 4 neighbours
@@ -1250,7 +1490,38 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
           const int64_t rr = own >= 0 ? own : a.cown[-1 - (int64_t)own];
           reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + rr * C::SB)[head] = make_float2(m, l);
         }
-        if (own < 0) {  // chunk of a heavy row/column: partial state for the merge kernel
+        if constexpr (C::MMA) {
+          // accumulators from the holder lanes' fragments (Mma::elem); chunks: fp32 partial states in the
+          // layout the merge kernels read
+          const int64_t ch = own < 0 ? -1 - (int64_t)own : 0;
+          if constexpr (PASS == 0) {
+            float lt = l + __shfl_xor_sync(kFull, l, 4);   // the head's sum over its 4 entry groups
+            lt += __shfl_xor_sync(kFull, lt, 8);
+            const bool first_u = mg.holder && mg.u == 0;
+            if (own < 0) {
+              float* pp = a.part + ch * (int64_t)(D + 2 * H);
+              st_pred(pp + D + 2 * mg.h, m, first_u);
+              st_pred(pp + D + 2 * mg.h + 1, lt, first_u);
+              mg.store_f32(pp, macc);
+            } else {
+              const float le = __shfl_sync(kFull, lt, mg.t), lo = __shfl_sync(kFull, lt, 16 + mg.t);
+              mg.store_bf16(a.out_a + r * RB, macc, 1.f / le, 1.f / lo);
+              st_pred(a.out_f + r * H + mg.h, (m + __log2f(lt)) * kLn2, first_u);
+            }
+          } else if constexpr (PASS == 1) {
+            if (own < 0) mg.store_f32(a.part + ch * (int64_t)D, macc);
+            else mg.store_bf16(a.out_a + r * RB, macc, a.scale, a.scale);
+          } else {
+            if (own < 0) {
+              float* pp = a.part + ch * (int64_t)(2 * D);
+              mg.store_f32(pp, macc);
+              mg.store_f32(pp + D, macc2);
+            } else {
+              mg.store_bf16(a.out_a + r * RB, macc, a.scale, a.scale);
+              mg.store_bf16(a.out_b + r * RB, macc2, 1.f, 1.f);
+            }
+          }
+        } else if (own < 0) {  // chunk of a heavy row/column: partial state for the merge kernel
           const int64_t ch = -1 - (int64_t)own;
           if constexpr (PASS == 0 && kBfly) l = Bfly<LPH>::all_sum(l);  // per lane group -> the row's (chunk's) l
           if constexpr (PASS == 0) {
@@ -1290,7 +1561,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<PASS, ES, D / 32>()))
       }
       // stage blocks other lanes read (entry state, stats) are refilled by the lanes that copy them:
       // order those reads before the new copies (formally, under independent thread scheduling)
-      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8) __syncwarp();
+      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8 || C::MMA) __syncwarp();
       md[s] = produce(s);   // refill the stage just consumed
       cp_commit();
     }
