@@ -285,6 +285,7 @@ def report_fields(per_step, stages, info, world, nnz, step_bytes, peak):
     t_exch = exch_ms / nsteps
     out = {
         "t_ms_mean": mean, "t_ms_min": min(per_step), "t_ms_std": statistics.pstdev(per_step),
+        "t_ms_steps": [round(x, 3) for x in per_step],
         "t_fwd_ms": stages["fwd"][0] / nsteps if "fwd" in stages else None,
         "t_bwd_ms": (stages["bwd_rows"][0] + stages["bwd_cols"][0]) / nsteps,
         "edges_per_s_per_gpu": nnz / (mean * 1e-3) / world,
