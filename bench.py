@@ -515,6 +515,13 @@ def run_ours(args):
     step_bytes = sum(per[s][0] * units[s][0] + per[s][1] * units[s][1] for s in per)
     roofline = physical_roofline(cfg, dom, stage_ms, per, units, compulsory_bytes(info, h, d, elt), peak, peak_src,
                                  world)
+    l2r = roofline.get("l2") if isinstance(roofline, dict) else None
+    if l2r and clk and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+        # the L2 -> SM interface moves 64 B/clk/SM: its peak scales with the SM clock, which the board's
+        # power limit lowers during sustained steps (profiles/r02/steptrace)
+        l2r["frac_at_sampled_sm_clock"] = l2r["achieved"] / (l2r["peak"] * clk["sm_mhz"] / clk["sm_max_mhz"])
+        l2r["note"] = ("frac: against the full-clock L2 -> SM peak; frac_at_sampled_sm_clock: against that peak "
+                       "scaled to the median SM clock sampled in the timed region")
 
     # ---- end to end through the C ABI with pinned host buffers ----
     e2e = None
