@@ -128,5 +128,34 @@ int main(int argc, char** argv) {
     printf("{\"mode\": \"gather\", \"ctas_per_sm\": %d, \"l2_read_gbs\": %.1f, \"buffer_mib\": %lld, \"best_ms\": %.4f, "
            "\"status\": \"%s\"}\n", ctas, moved / (best * 1e-3) / 1e9, (long long)mib, best, cudaGetErrorString(e));
   }
+  // sustained gather: back-to-back launches for `sustain_s` seconds (argv[3], 0 = skip), the board's power
+  // limit applying (run next to an nvidia-smi trace); reported per 0.25-s window
+  const double sustain_s = argc > 3 ? atof(argv[3]) : 0.0;
+  if (sustain_s > 0) {
+    const int ctas = 12, grid = sms * ctas, smem = 4 * 2 * 4 * 512;
+    const uint32_t rows = (uint32_t)(bytes / 512);
+    const int iters = (int)((int64_t)passes * rows / 4 / ((int64_t)grid * 4)) + 1;
+    const double moved = (double)grid * 4 * iters * 4 * 512;
+    double t = 0, wt = 0, wb = 0;
+    int win = 0;
+    while (t < sustain_s * 1e3) {
+      cudaEventRecord(a);
+      gather_rd<<<grid, 128, smem>>>(p, rows, iters, sink);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      t += ms;
+      wt += ms;
+      wb += moved;
+      if (wt >= 250.0) {
+        printf("{\"mode\": \"gather_sustained\", \"window\": %d, \"t_ms\": %.0f, \"l2_read_gbs\": %.1f}\n", win++, t,
+               wb / (wt * 1e-3) / 1e9);
+        wt = 0;
+        wb = 0;
+      }
+    }
+    ok &= cudaGetLastError() == cudaSuccess;
+  }
   return ok ? 0 : 1;
 }
