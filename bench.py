@@ -69,13 +69,16 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback"
 
 
-def alg_bytes(h, d, elt):
+def alg_bytes(h, d, elt, colfirst=False):
     """SURVEY.md 8(d) no-reuse gather model: algorithmic bytes per edge and per row of each pass.
-    I = 4 B column/row index, R = 4 B row offset, D = h*d, b = dtype bytes."""
+    I = 4 B column/row index, R = 4 B row offset, D = h*d, b = dtype bytes.  Column-first backward
+    (gt_plan_info.bwd_colfirst): the row pass gathers k_j alone; dP moves to the column pass, which uses
+    its own v_j."""
     D, I, R = h * d, 4, 4
+    rows = (I + D * elt, R + 2 * D * elt) if colfirst else (I + 2 * D * elt, R + 3 * D * elt + 8 * h)
     return {
         "fwd": (I + 2 * D * elt, R + 2 * D * elt + 4 * h),          # k_j, v_j | q in, y out, lse out
-        "bwd_rows": (I + 2 * D * elt, R + 3 * D * elt + 8 * h),     # k_j, v_j | q, dy in, dq out, lse in, D out
+        "bwd_rows": rows,          # k_j [, v_j] | [q, dy in,] dq out [, lse in, D out]
         "bwd_cols": (I + 2 * D * elt + 8 * h, R + 4 * D * elt),     # q_i, dy_i, lse_i, D_i | k, v in, dk, dv out
     }
 
@@ -92,6 +95,14 @@ def compulsory_bytes(info, h, d, elt):
     s2 = E * h * 4 if es else 0
     pd = E * h * (4 if elt == 2 else 8) if es else 0
     item = 20 * N                                  # work-item tables (begin, end, owner) per row
+    if info.get("bwd_colfirst"):
+        ds = E * h * elt                           # dS per entry and head (column pass -> row pass)
+        st = N * 8 * h                             # (LSE2, D) per row
+        return {
+            "fwd": 3 * row + row + N * h * 4 + 4 * E + item + s2,
+            "bwd_rows": row + row + 4 * E + item + ds,                                   # k in, dq out, dS in
+            "bwd_cols": 2 * row + 2 * row + 4 * Ein + item + 4 * Ein + s2 + st + ds,     # q dy k v in, dk dv out
+        }
     return {
         "fwd": 3 * row + row + N * h * 4 + 4 * E + item + s2,                       # q k v in, y lse out, s2 out
         "bwd_rows": 4 * row + N * h * 4 + row + N * 8 * h + 4 * E + item + s2 + pd,  # k v dy y lse in, dq D out
@@ -508,7 +519,7 @@ def run_ours(args):
     # ---- roofline of the dominant kernel stage (per launch, device-timed on the launching stream) ----
     stage_ms = {s: (stages[s][0] / max(stages[s][1], 1)) for s in ("fwd", "bwd_rows", "bwd_cols")}
     dom = max(stage_ms, key=stage_ms.get)
-    per = alg_bytes(h, d, elt)
+    per = alg_bytes(h, d, elt, bool(info.get("bwd_colfirst")))
     units = {"fwd": (info["nnz_local"], info["n_local"]), "bwd_rows": (info["nnz_local"], info["n_local"]),
              "bwd_cols": (info["nnz_in_local"], info["n_local"])}
     peak, peak_src = peaks()
@@ -587,7 +598,8 @@ def run_ours(args):
                        "edge_state": info["edge_state"], "edge_state_bytes": info["edge_state_bytes"],
                        "bwd_mode": info["bwd_mode"], "transport": info["transport"],
                        "kv_fp8": info["kv_fp8"], "hot_cols": info["hot_cols"],
-                       "hot_entries": info["hot_entries"]},
+                       "hot_entries": info["hot_entries"],
+                       "bwd_order": "column-first" if info.get("bwd_colfirst") else "row-first"},
             "roofline": roofline,
             # whole step: ncu DRAM bytes of the three passes over the step time (physical), and the
             # no-reuse gather model (exceeds 1 on L2-local graphs: a model, not a fraction of the peak)

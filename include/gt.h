@@ -209,6 +209,10 @@ typedef struct {
   int64_t kv_fp8_bytes;           /* device bytes of that table */
   int64_t hot_cols;               /* columns in the hot-column table (gt_opts.hot_cols) */
   int64_t hot_entries;            /* owned-row entries that read it */
+  int bwd_colfirst;               /* 1: a backward of the last forward runs column-first (world 1, stored
+                                     logits): (LSE2, D) of every row, the column pass (dP with its own v_j,
+                                     dK, dV, dS per entry), then a row pass gathering k_j alone (dQ);
+                                     GT_COLFIRST=0 selects the row-first order */
 } gt_plan_info;
 
 /* Fills *o with defaults: rank 0, world-1 comm, bf16, scale 0, GT_AUTO, validate 1,

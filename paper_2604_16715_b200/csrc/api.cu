@@ -381,6 +381,10 @@ static void fill_info(gt_plan_s* P, int64_t nrc, int64_t ncc) {
   I.hot_cols = P->n_hot;
   I.hot_entries = P->hot_entries;
   if (P->n_hot) I.launches_fwd += 1;                    // + the hot-table pack
+  // column-first backward (a backward of the last forward, world 1): + the (LSE2, D) kernel
+  I.bwd_colfirst = single && P->colfirst && P->es_logits && !P->kv_fp8 && !P->n_hot &&
+                   P->heads * (P->dtype == GT_F32 ? 4 : 2) >= 4;
+  if (I.bwd_colfirst) I.launches_bwd += 1;
   int64_t dev = 0;
   for (const DevBuf* b : {&P->d_row_ptr, &P->d_col, &P->d_col_ptr, &P->d_row, &P->d_stats, &P->d_part_fwd,
                           &P->d_part_rowb, &P->d_part_colb, &P->d_send_out_idx, &P->d_send_in_idx, &P->d_send_buf,
@@ -940,6 +944,8 @@ static gt_status plan_impl(const gt_csr* csr, int64_t n, int64_t nnz, int heads,
       P->es = misfit == 0;
       P->es_logits = P->es && logits;
       P->info.edge_state_bytes = P->es ? es_bytes : 0;
+      const char* cf = std::getenv("GT_COLFIRST");  // backward order at world 1 (A/B switch; default column-first)
+      P->colfirst = !(cf && cf[0] == '0');
     }
     if (P->es) {
       if (P->es_logits) GT_TRY(P->d_s2.alloc(std::max<size_t>((size_t)P->nnz_local, 1) * heads * sizeof(float)));
@@ -1341,6 +1347,19 @@ static gt_status attn_bwd_eager(gt_plan_t P, const void* q, const void* k, const
     P->mark_begin(4, st, &ev);
     GT_TRY(launch_bwd_cols_peer(P, q, k, v, dy, dk, dv, st));
     P->mark_end(4, st, ev);
+    return GT_OK;
+  }
+  if (!multi && P->colfirst && P->es_logits && fresh && !stale && !P->kv_fp8 && !P->n_hot &&
+      P->heads * (P->dtype == GT_F32 ? 4 : 2) >= 4) {
+    // Column-first order (world 1, this forward's logits stored): the column pass computes dP with its own
+    // v_j and stores dS, so the row pass gathers k_j alone (2 KB -> 1.5 KB of gathered rows per entry)
+    P->mark_begin(4, st, &ev);
+    GT_TRY(launch_bwd_cf_cols(P, q, k, v, y, lse, dy, dk, dv, st));
+    P->mark_end(4, st, ev);
+    P->mark_begin(2, st, &ev);
+    GT_TRY(launch_bwd_cf_rows(P, q, k, v, lse, dy, dq, st));
+    if (P->ev_dq_ready) GT_TRY(record_external(P->ev_dq_ready, st));
+    P->mark_end(2, st, ev);
     return GT_OK;
   }
   if (multi) {

@@ -489,6 +489,46 @@ gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void
   return GT_OK;
 }
 
+// Column-first backward, column half: (LSE2, D) of every row, then the column pass over A^T computing
+// dP = <dY_i, v_j> with its own v_j (the row pass of the row-first order gathers v_j for it), P from the
+// forward's logit, dS; it stores dS per entry in CSR order for the row half.  Bytes per entry: q_i, dY_i,
+// (LSE2, D)_i, the logit; the row half then gathers k_j and dS alone.
+gt_status launch_bwd_cf_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* y,
+                             const float* lse, const void* dy, void* dk, void* dv, cudaStream_t st) {
+  GT_TRY(row_stats(P->dtype, P->heads, P->heads * P->d, y, dy, lse, P->n_local, P->d_stats.as<float>(),
+                   (int)P->st_row_bytes, st));
+  EntryState e;
+  e.mode = 1;
+  e.in = P->d_s2.as<float>();
+  e.out = P->d_pd.as<float>();
+  e.src = P->d_src.as<int32_t>();
+  GT_TRY(pipe_pass(P, 2, P->w_cols, P->heavy_cols, P->d_part_colb.as<float>(), k, v, nullptr, q, dy, nullptr, nullptr,
+                   dk, dv, nullptr, st, 0, e));
+  if (P->heavy_cols.nchunks() > 0) {
+    MergeArgs m = merge_args(P->heavy_cols, P->d_part_colb, P->scale);
+    m.dk = (char*)dk;
+    m.dv = (char*)dv;
+    GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 2, m, st));
+  }
+  return GT_OK;
+}
+
+// Column-first backward, row half: dQ_i = scale sum_e dS_e k_j with the column half's dS.
+gt_status launch_bwd_cf_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const float* lse,
+                             const void* dy, void* dq, cudaStream_t st) {
+  EntryState e;
+  e.mode = 1;
+  e.in = P->d_pd.as<float>();
+  GT_TRY(pipe_pass(P, 1, P->w_rows, P->heavy_rows, P->d_part_rowb.as<float>(), q, dy, lse, k, v, nullptr, nullptr, dq,
+                   nullptr, P->d_stats.as<float>(), st, 0, e));
+  if (P->heavy_rows.nchunks() > 0) {
+    MergeArgs m = merge_args(P->heavy_rows, P->d_part_rowb, P->scale);
+    m.dq = (char*)dq;
+    GT_TRY(merge(P->dtype, P->heads, P->heads * P->d, 1, m, st));
+  }
+  return GT_OK;
+}
+
 // Reduce-scatter backward, sender side: the column pass over the halo columns (local rows' entries
 // with remote columns, grouped by slot; own k, v = the [k | v] rows received in the forward), every
 // piece a chunk partial, then summed per slot into the send rows.

@@ -179,12 +179,17 @@ struct PC {
   static constexpr int PDB = sizeof(T) == 2 ? 4 : 8;      // stored (P, dS) of one entry and head: bf16x2 | f32x2
   // the recompute column pass gathers each in-neighbour's (LSE2, D) block; with stored (P, dS) it does not
   static constexpr bool STATS = PASS == 2 && !(ES & 1);
+  // ES bit 8: column-first backward (PArgs::mode 1, launch_bwd_colfirst): the column pass gathers q_i,
+  // dY_i and (LSE2, D)_i, reads the forward's logit through the CSC -> CSR map, computes dP with its own
+  // v_j and stores dS per entry (CSR order); the row pass then gathers k_j alone and reads that dS
+  static constexpr bool CF = (ES & 8) != 0;
+  static constexpr int ESZ = (int)sizeof(T);              // bytes of a stored dS (column-first)
   // own slot: fwd q | rowb [q] dY Y lse | colb [k v]   (the row pass recomputing q.k needs q; with
   // stored (P, dS) the column pass needs no own-column data)
   static constexpr int OWN_DY = PASS == 1 ? ((ES & 2) ? 0 : RB) : 0;
   static constexpr int OWN_Y = OWN_DY + RB;
   static constexpr int OWN_LSE = OWN_Y + RB;   // the row's LSE of the lane's head, one 4-byte slot per lane
-  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? OWN_LSE + 4 * 32 : ((ES & 1) ? 0 : 2 * RB));
+  static constexpr int OWN = PASS == 0 ? RB : (PASS == 1 ? (CF ? 0 : OWN_LSE + 4 * 32) : ((ES & 1) ? 0 : (CF ? RB : 2 * RB)));
 #ifdef GT_PIPE_U  // tuning override (A/B builds)
   static constexpr int U = RB >= 2048 ? 1 : (RB >= 1024 ? 2 : (GT_PIPE_U * H <= 32 ? GT_PIPE_U : 32 / H));
 #else
@@ -194,11 +199,13 @@ struct PC {
 #endif
   // per-stage entry state gathered into the stage (ES): rowb s2[U][H] f32 (the forward's logits),
   // colb (P, dS)[U][H] (the row pass's)
-  static constexpr int AUX = PASS == 1 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 2 && (ES & 1)) ? U * H * PDB : 0);
+  // (column-first: rowb dS[U][H] (T); colb s2[U][H] f32 + the U entries' CSR positions)
+  static constexpr int AUX = PASS == 1 ? (CF ? U * H * ESZ : ((ES & 2) ? U * H * 4 : 0))
+                                       : ((PASS == 2 && (ES & 1)) ? U * H * PDB : ((PASS == 2 && CF) ? U * H * 4 + U * 4 : 0));
   // TMA gathers (sm_100 cp.async.bulk.tensor tile::gather4: 4 rows of a 2-D tensor map per instruction)
   // for the two feature rows of every neighbour when the stage holds exactly 4 neighbours; the
   // stage then keeps the 4 first rows (k | q) contiguous, then the 4 second rows (v | dY), then stats
-  static constexpr bool TMA = GT_PIPE_TMA && U == 4 && !F8;
+  static constexpr bool TMA = GT_PIPE_TMA && U == 4 && !F8 && !CF;
   // Tensor-core consumer (Mma below): the stage's dot products and SpMM updates as mma.sync m16n8k16
   // products for the products shape (bf16, 4 heads of 64, 4 neighbours per stage) - the forward, the
   // row pass reading the forward's logits and the column pass reading the stored (P, dS)
@@ -206,12 +213,13 @@ struct PC {
                               (PASS == 0 || (PASS == 1 && (ES & 2)) || (PASS == 2 && (ES & 1)));
   // bytes per neighbour in a stage; the tensor-core layout pads it to 32 mod 128 so that the 8 rows one
   // ldmatrix phase reads (4 neighbours x 2 heads) fall in 8 distinct 16-byte bank groups
-  static constexpr int EB = (F8 ? GR : 2 * RB + (STATS ? SB : 0)) + (MMA ? 32 : 0);
+  static constexpr int EB = (F8 ? GR : ((PASS == 1 && CF) ? RB : 2 * RB + (STATS ? SB : 0))) + (MMA ? 32 : 0);
   static constexpr int STAGE = (U * EB + AUX + 127) / 128 * 128;   // 128-byte aligned TMA destinations
   static constexpr int OWNP = (OWN + 15) / 16 * 16;
   // ES transpose scratch of the per-stage store: fwd s2[U][H], rowb (P, dS)[U][H]
   // (the tensor-core consumer stores them from the registers of the lanes holding them: no scratch)
-  static constexpr int XS = MMA ? 0 : (PASS == 0 ? ((ES & 2) ? U * H * 4 : 0) : ((PASS == 1 && (ES & 1)) ? U * H * PDB : 0));
+  static constexpr int XS = MMA ? 0 : (PASS == 0 ? ((ES & 2) ? U * H * 4 : 0)
+                                                 : ((PASS == 1 && (ES & 1)) ? U * H * PDB : ((PASS == 2 && CF) ? U * H * ESZ : 0)));
   static constexpr int kS = stages_of<PASS, ES>();                   // stages per warp
   static constexpr int MB = TMA ? kS * 8 : 0;                       // one mbarrier per stage
   static constexpr int WARP_SMEM = (kS * (STAGE + OWNP + XS) + MB + 127) / 128 * 128;
@@ -265,6 +273,7 @@ struct PArgs {
   const int* kvref;      // fp8 gathers: {E_k, E_v} = max exponent of the K / V scales over the table
   const void* win;       // persisting L2 access-policy window of the launch (hot-column table), or null
   int64_t win_bytes;
+  int mode;              // 1: column-first backward (EntryState::mode; selects the ES bit 8 kernels)
   uint32_t rb, rb2, sb;  // row strides (bytes) of the gathered tables as run-time values: a row address is
                          // then one IMAD.WIDE.U32 (an immediate power-of-two stride becomes shift + high +
                          // two 64-bit adds)
@@ -580,6 +589,17 @@ __device__ __forceinline__ int to_f16_norm(const uint32_t (&w)[EPL / 2], uint32_
   return e;
 }
 
+// predicated 32-bit shared store (generic address of a shared location)
+__device__ __forceinline__ void sts_pred_u32(void* p, uint32_t x, bool on) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;}" ::"r"(su32(p)), "r"(x),
+               "r"((int)on) : "memory");
+}
+// predicated 16-bit global store of raw bits
+__device__ __forceinline__ void st_pred_u16(void* p, uint16_t x, bool on) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b16 [%0], %1;}" ::"l"(p), "h"(x),
+               "r"((int)on) : "memory");
+}
+
 // predicated 32-bit global store of raw bits
 __device__ __forceinline__ void st_pred_u32(uint32_t* p, uint32_t x, bool on) {
   asm volatile("{.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;}" ::"l"(p), "r"(x),
@@ -790,10 +810,14 @@ struct Meta {      // warp-uniform description of one filled stage
 #ifndef GT_MMA_BWD_MINB  // tensor-core backward passes: resident CTAs per SM (register cap)
 #define GT_MMA_BWD_MINB 5
 #endif
+#ifndef GT_CF_COLB_MINB  // column-first column pass: resident CTAs per SM (register cap)
+#define GT_CF_COLB_MINB 5
+#endif
 template <typename T, int H, int D, int PASS, int ES>
 constexpr int min_ctas() {
   constexpr int EPL = D / 32;
   return EPL > 8 ? 1
+                 : ((ES & 8) && PASS == 2) ? GT_CF_COLB_MINB
                  : ((ES & 4) ? 5
                              : (PASS == 0 ? GT_FWD_MINB
                                           : (PC<T, H, D, PASS, ES>::MMA ? GT_MMA_BWD_MINB
@@ -881,7 +905,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
     win_base = base;
     win = (base + lane < nnbr) ? __ldg(a.nbr + base + lane) : 0;
     win_next = (base + 32 + lane < nnbr) ? __ldg(a.nbr + base + 32 + lane) : 0;
-    if constexpr ((ES & 1) && PASS == 2) {
+    if constexpr ((ES & 9) && PASS == 2) {
       wsrc = (base + lane < nnbr) ? __ldg(a.src + base + lane) : 0;
       wsrc_next = (base + 32 + lane < nnbr) ? __ldg(a.src + base + 32 + lane) : 0;
     }
@@ -943,7 +967,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
       win_base += 32;
       win = win_next;
       win_next = (win_base + 32 + lane < nnbr) ? __ldg(a.nbr + win_base + 32 + lane) : 0;
-      if constexpr ((ES & 1) && PASS == 2) {
+      if constexpr ((ES & 9) && PASS == 2) {
         wsrc = wsrc_next;
         wsrc_next = (win_base + 32 + lane < nnbr) ? __ldg(a.src + win_base + 32 + lane) : 0;
       }
@@ -1017,7 +1041,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
       }
       char* dst = st + u * EB + lane * LB;
       cp_lane_z<LB>(dst, pa, valid);
-      cp_lane_z<LB>(dst + RB, pb, valid);
+      if constexpr (!(PASS == 1 && C::CF)) cp_lane_z<LB>(dst + RB, pb, valid);
       // (LSE2, D) block of the neighbour: SB / 16 lanes copy 16 bytes each (read by all lanes of a head
       // after the stage's wait + __syncwarp)
       if constexpr (C::STATS) {
@@ -1040,6 +1064,23 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
         else cp_async4z(st + U * EB + lane * 4, src, ku < cnt);
       }
     }
+    if constexpr (C::CF && PASS == 1) {  // dS of the stage's entries (contiguous, CSR order), stored by the column pass
+      constexpr int EW = H * C::ESZ / 4;   // words per entry (the host selects these kernels for H * ESZ >= 4)
+      const bool kv = lane < cnt * EW;
+      if (lane < U * EW)
+        cp_async4z(st + U * EB + lane * 4,
+                   row_addr(reinterpret_cast<const char*>(a.es_in), (uint32_t)pe * EW + (kv ? lane : 0), 4), kv);
+    }
+    if constexpr (C::CF && PASS == 2) {
+      // the forward's base-2 logits of the stage's entries through the CSC -> CSR map, and (plain shared
+      // stores, ordered before the consumer by its __syncwarp) the entries' CSR positions for the dS store
+      const int ku = lane / H, kh = lane % H;
+      const uint32_t ke = (uint32_t)__shfl_sync(kFull, wsrc, off + ku);
+      const char* src = row_addr(reinterpret_cast<const char*>(a.es_in) + kh * 4, ku < cnt ? ke : 0u, H * 4);
+      if (lane < U * H) cp_async4z(st + U * EB + lane * 4, src, ku < cnt);
+      const uint32_t pu = (uint32_t)__shfl_sync(kFull, wsrc, off + (lane & (U - 1)));
+      sts_pred_u32(st + U * EB + U * H * 4 + lane * 4, pu, lane < U);
+    }
     md.e0 = pe;
     md.cnt = cnt;
     md.own = cur_own;
@@ -1051,10 +1092,14 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
       if constexpr (PASS == 0) {
         cp_slice<LB>(o, a.oa + r * RB, lane);
       } else if constexpr (PASS == 1) {
-        if constexpr (!(ES & 2)) cp_slice<LB>(o, a.oa + r * RB, lane);
-        cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
-        cp_slice<LB>(o + C::OWN_Y, a.oc + r * RB, lane);
-        cp_async<4>(o + C::OWN_LSE + lane * 4, a.lse + r * H + head);  // distinct slots: no same-address writes
+        if constexpr (!C::CF) {  // (the column-first row pass needs no own-row data)
+          if constexpr (!(ES & 2)) cp_slice<LB>(o, a.oa + r * RB, lane);
+          cp_slice<LB>(o + C::OWN_DY, a.ob + r * RB, lane);
+          cp_slice<LB>(o + C::OWN_Y, a.oc + r * RB, lane);
+          cp_async<4>(o + C::OWN_LSE + lane * 4, a.lse + r * H + head);  // distinct slots: no same-address writes
+        }
+      } else if constexpr (C::CF) {  // column-first column pass: v_j (dP = <dY_i, v_j>)
+        cp_slice<LB>(o, a.ob + r * a.own_stride, lane);
       } else if constexpr (!(ES & 1)) {
         cp_slice<LB>(o, a.oa + r * a.own_stride, lane);
         cp_slice<LB>(o + RB, a.ob + r * a.own_stride, lane);
@@ -1077,6 +1122,21 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
   float fo = 1.f, ifo = 1.f, fq = 1.f;
   const float rk = C::F8 ? exp2i(__ldg(a.kvref)) : 1.f, rv = C::F8 ? exp2i(__ldg(a.kvref + 1)) : 1.f;
   const float irk = 1.f / rk, irv = 1.f / rv;
+  // column-first column pass, butterfly layout: per-lane constants (byte offsets in a stage of the lane
+  // group's (LSE2, D) and logit, the dS store's source lane, CSR-position slot and head offset)
+  int cf_ug = 0, cf_sd = 0, cf_s2 = 0, cf_src = 0, cf_pos = 0, cf_eo = 0;
+  int cf_w[4] = {0, 0, 0, 0};
+  if constexpr (C::CF && PASS == 2 && U == 4 && LPH >= 4) {
+    cf_ug = Bfly<LPH>::group(lane);
+    cf_sd = cf_ug * EB + 2 * RB + head * 8;
+    cf_s2 = U * EB + (cf_ug * H + head) * 4;
+    const int f = lane < U * H ? lane : 0;
+    cf_src = Bfly<LPH>::src(LPH * (f % H), f / H);
+    cf_pos = U * EB + U * H * 4 + (f / H) * 4;
+    cf_eo = (f % H) * C::ESZ;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cf_w[u] = Bfly<LPH>::src(lane, u);
+  }
   // tensor-core consumer: lane geometry, own-row B fragments, accumulators (Mma)
   Mma mg;
   if constexpr (C::MMA) mg.init<EB>(lane);
@@ -1095,7 +1155,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
 #pragma unroll
     for (int s = 0; s < kS; ++s) {
       cp_wait<kS - 1>();
-      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8 || C::MMA) __syncwarp();  // blocks copied by other lanes
+      if constexpr (PASS == 2 || (PASS == 1 && ((ES & 2) || C::CF)) || C::F8 || C::MMA) __syncwarp();  // blocks copied by other lanes
       const Meta cur = md[s];
       if (cur.cnt == 0) return;  // stages are consumed in order: nothing after an empty one (no copy in flight)
       if constexpr (kTma) {
@@ -1138,6 +1198,9 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
           for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
           m = -INFINITY;
           l = 0.f;
+        } else if constexpr (PASS == 1 && C::CF) {
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
         } else if constexpr (PASS == 1) {
           if constexpr (!(ES & 2)) lds_raw<W>(o + lane * LB, ow2);
           lds_raw<W>(o + C::OWN_DY + lane * LB, ow);
@@ -1155,7 +1218,9 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
 #pragma unroll
           for (int i = 0; i < EPL; ++i) acc[i] = 0.f;
         } else {
-          if constexpr (!(ES & 1)) {
+          if constexpr (C::CF) {
+            lds_raw<W>(o + lane * LB, ow2);      // v_j
+          } else if constexpr (!(ES & 1)) {
             lds_raw<W>(o + lane * LB, ow);       // k_j
             lds_raw<W>(o + RB + lane * LB, ow2); // v_j
           }
@@ -1214,6 +1279,102 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
         const uint32_t d0 = mg.b0on ? __byte_perm(wa, wb, 0x7632) : 0u, d1 = mg.b1on ? __byte_perm(wc, wd, 0x7632) : 0u;
         mg.spmm(sa + RB + mg.off_sp, p0, p1, macc2);
         mg.spmm(sa + mg.off_sp, d0, d1, macc);
+      } else if constexpr (C::CF && PASS == 1) {
+        // Column-first row pass: dQ_i += dS_e k_j with the column pass's dS (masked neighbours: zero-filled
+        // rows and weights)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t kw[W];
+          lds_raw<W>(st + u * EB + lane * LB, kw);
+          uint32_t w;
+          if constexpr (sizeof(T) == 2) w = reinterpret_cast<const uint16_t*>(st + U * EB)[u * H + head];
+          else w = reinterpret_cast<const uint32_t*>(st + U * EB)[u * H + head];
+          accum<T, W, EPL>(w, kw, acc);
+        }
+      } else if constexpr (C::CF && PASS == 2) {
+        // Column-first column pass: dP_e = <dY_i, v_j> with the column's own v_j,
+        // P_e = 2^(s2_e - LSE2_i) from the forward's logit, dS_e = P_e (dP_e - D_i); dV_j += P_e dY_i,
+        // dK_j += dS_e q_i (unscaled; weights rounded to T as in the stored-state pass); dS_e is stored at
+        // the entry's CSR position for the row pass (rounded to T: the row pass's dQ weight)
+        const float* s2x = reinterpret_cast<const float*>(st + U * EB);
+        const uint32_t* pos = reinterpret_cast<const uint32_t*>(st + U * EB + U * H * 4);
+        T* xd = reinterpret_cast<T*>(xs + s * C::XS);
+        if constexpr (U == 4 && LPH >= 4) {
+          using B = Bfly<LPH>;
+          float part[4];
+          uint32_t gws[4][W];   // dY_i slices, kept for dV (no second load)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            lds_raw<W>(st + C::template voff<false>(u) + lane * LB, gws[u]);
+            part[u] = dot_raw<T, W>(gws[u], ow2);
+          }
+          const float dpl = B::reduce(part, lane);
+          const float2 sd = *reinterpret_cast<const float2*>(st + cf_sd);
+          const float pl = cf_ug < cnt ? ex2(*reinterpret_cast<const float*>(st + cf_s2) - sd.x) : 0.f;
+          const float dsl = pl * (dpl - sd.y);
+          {  // dS of the stage's entries to their CSR positions: lane f = u H + h, from a lane holding it
+            const float x = __shfl_sync(kFull, dsl, cf_src);
+            char* dst = const_cast<char*>(row_addr(reinterpret_cast<const char*>(a.es_out) + cf_eo,
+                                                   *reinterpret_cast<const uint32_t*>(st + cf_pos), H * C::ESZ));
+            if constexpr (sizeof(T) == 2)
+              st_pred_u16(dst, __bfloat16_as_ushort(__float2bfloat16_rn(x)), lane < cnt * H);
+            else
+              st_pred_u32(reinterpret_cast<uint32_t*>(dst), __float_as_uint(x), lane < cnt * H);
+          }
+          if constexpr (sizeof(T) == 2) {
+            const uint32_t wl = pack_pd_bf16(pl, dsl);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t e = __shfl_sync(kFull, wl, cf_w[u]);
+              uint32_t qw[W];
+              lds_raw<W>(st + C::template koff<false>(u) + lane * LB, qw);
+              accum<T, W, EPL, false>(e, gws[u], acc2);  // P (low half)
+              accum<T, W, EPL, true>(e, qw, acc);        // dS (high half)
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float pu = __shfl_sync(kFull, pl, cf_w[u]);
+              const float du = __shfl_sync(kFull, dsl, cf_w[u]);
+              uint32_t qw[W];
+              lds_raw<W>(st + C::template koff<false>(u) + lane * LB, qw);
+              const uint32_t (&gw)[W] = gws[u];
+              accum<T, W, EPL>(__float_as_uint(pu), gw, acc2);
+              accum<T, W, EPL>(__float_as_uint(du), qw, acc);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            uint32_t qw[W], gw[W];
+            lds_raw<W>(st + C::template koff<false>(u) + lane * LB, qw);
+            lds_raw<W>(st + C::template voff<false>(u) + lane * LB, gw);
+            const float2 sd = reinterpret_cast<const float2*>(st + C::template soff<false>(u))[head];
+            const float dp = head_sum<LPH>(dot_raw<T, W>(gw, ow2));
+            const float p = u < cnt ? ex2(s2x[u * H + head] - sd.x) : 0.f;
+            const float ds = p * (dp - sd.y);
+            xd[u * H + head] = T(ds);   // all lanes of a head write the same value
+            if constexpr (sizeof(T) == 2) {
+              const uint32_t e = pack_pd_bf16(p, ds);
+              accum<T, W, EPL, false>(e, gw, acc2);
+              accum<T, W, EPL, true>(e, qw, acc);
+            } else {
+              accum<T, W, EPL>(__float_as_uint(p), gw, acc2);
+              accum<T, W, EPL>(__float_as_uint(ds), qw, acc);
+            }
+          }
+        }
+        // (head_sum branch) dS of the stage's entries to their CSR positions: lane f = u H + h stores one
+        if constexpr (!(U == 4 && LPH >= 4)) {
+          __syncwarp();
+          const int f = lane < U * H ? lane : 0;
+          if constexpr (sizeof(T) == 2)
+            st_pred_u16(reinterpret_cast<uint16_t*>(a.es_out) + (int64_t)pos[f / H] * H + f % H,
+                        reinterpret_cast<const uint16_t*>(xd)[f], lane < cnt * H);
+          else
+            st_pred_u32(reinterpret_cast<uint32_t*>(a.es_out) + (int64_t)pos[f / H] * H + f % H,
+                        reinterpret_cast<const uint32_t*>(xd)[f], lane < cnt * H);
+        }
       } else if constexpr (C::F8 && PASS == 0) {
         // fp8 forward: s = qscale 2^eq 2^ek_j <q', k8_j>, p~ = 2^(s - m), acc += f16(p~ 2^(ev_j - E_v)) v8_j
         // (y = acc 2^E_v / l); the dots are reduce-scattered by the butterfly as in the bf16 path, in
@@ -1486,7 +1647,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
       if (cur.last) {
         const int32_t own = cur.own;
         const int64_t r = own >= 0 ? own : 0;
-        if constexpr (PASS == 1) {  // (LSE2, D) of the row (every chunk of a heavy row writes the same values)
+        if constexpr (PASS == 1 && !C::CF) {  // (LSE2, D) of the row (every chunk of a heavy row writes the same values)
           const int64_t rr = own >= 0 ? own : a.cown[-1 - (int64_t)own];
           reinterpret_cast<float2*>(reinterpret_cast<char*>(a.out_f) + rr * C::SB)[head] = make_float2(m, l);
         }
@@ -1561,7 +1722,7 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
       }
       // stage blocks other lanes read (entry state, stats) are refilled by the lanes that copy them:
       // order those reads before the new copies (formally, under independent thread scheduling)
-      if constexpr (PASS == 2 || (PASS == 1 && (ES & 2)) || C::F8 || C::MMA) __syncwarp();
+      if constexpr (PASS == 2 || (PASS == 1 && ((ES & 2) || C::CF)) || C::F8 || C::MMA) __syncwarp();
       md[s] = produce(s);   // refill the stage just consumed
       cp_commit();
     }
@@ -1588,6 +1749,35 @@ __global__ void __launch_bounds__(256) fill_empty_kernel(const int32_t* ids, int
         reinterpret_cast<float2*>(reinterpret_cast<char*>(out_f) + r * sb)[lane] = make_float2(-INFINITY, 0.f);
     }
   }
+}
+
+// (LSE2, D) of every row for the column-first backward (D_i = sum_e P_e dP_e =
+// <dY_i, Y_i> since sum_e P_e = 1), the values the row pass of the row-first order writes (same products,
+// same order); rows without entries get (-inf, 0) (their LSE is -inf, their Y 0).  One warp per row.
+template <typename T, int H, int D>
+__global__ void __launch_bounds__(256) row_stats_kernel(const char* y, const char* dy, const float* lse, int64_t n,
+                                                        char* stats, int sb) {
+  using C = PC<T, H, D, 1, 0>;
+  constexpr int W = C::W, LB = C::LB, LPH = C::LPH, RB = C::RB;
+  const int lane = threadIdx.x & 31, head = lane / LPH;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    uint32_t yw[W], gw[W];
+    lds_raw<W>(y + r * RB + lane * LB, yw);
+    lds_raw<W>(dy + r * RB + lane * LB, gw);
+    const float d = head_sum<LPH>(dot_raw<T, W>(gw, yw));
+    if (lane % LPH == 0) reinterpret_cast<float2*>(stats + r * sb)[head] = make_float2(lse[r * H + head] * kLog2e, d);
+  }
+}
+
+template <typename T, int H, int D>
+gt_status row_stats_run(const void* y, const void* dy, const float* lse, int64_t n, float* stats, int sb,
+                        cudaStream_t st) {
+  if (n <= 0) return GT_OK;
+  const int blocks = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 8);
+  row_stats_kernel<T, H, D><<<blocks, 256, 0, st>>>((const char*)y, (const char*)dy, lse, n, (char*)stats, sb);
+  GT_CUDA_TRY(cudaGetLastError());
+  return GT_OK;
 }
 
 gt_status fill_empty(int pass, const int32_t* ids, int64_t n, char* out_a, char* out_b, float* out_f, int64_t rb,
@@ -1776,6 +1966,13 @@ struct Ops {
   // ES bits: 1 = (P, dS) materialised (rowb stores, colb reads), 2 = logits materialised (fwd stores,
   // rowb reads)
   static gt_status run(int pass, const PArgs& a, cudaStream_t st, int rs) {
+    if (a.mode == 1) {  // column-first backward (world 1, stored logits; dS rows of >= 4 bytes per entry)
+      if constexpr (H * sizeof(T) >= 4) {
+        if (pass == 1) return launch<T, H, D, 1, false, 8>(a, st, rs);
+        if (pass == 2) return launch<T, H, D, 2, false, 8>(a, st, rs);
+      }
+      return fail(GT_ECONFIG, "column-first backward: unsupported pass / shape");
+    }
     if (a.kvref) {  // fp8 K||V gathers (world 1, bf16, heads * d >= 128)
       if constexpr (sizeof(T) == 2 && D >= 128) {
         if (pass == 0) return a.es_out ? launch<T, H, D, 0, false, 6>(a, st, rs) : launch<T, H, D, 0, false, 4>(a, st, rs);
@@ -1825,7 +2022,28 @@ gt_status dispatch(int dtype, int H, int D, int pass, const PArgs& a, cudaStream
   return fail(GT_ECONFIG, "unsupported (dtype, heads, heads*d)");
 }
 
+gt_status row_stats_dispatch(int dtype, int H, int D, const void* y, const void* dy, const float* lse, int64_t n,
+                             float* stats, int sb, cudaStream_t st) {
+#define GT_CASE(TT, HH, DD) \
+  if (H == HH && D == DD) return row_stats_run<TT, HH, DD>(y, dy, lse, n, stats, sb, st);
+#define GT_HCASES(TT)                                                                              \
+  GT_CASE(TT, 1, 64) GT_CASE(TT, 2, 64) GT_CASE(TT, 4, 64) GT_CASE(TT, 8, 64)                        \
+  GT_CASE(TT, 1, 128) GT_CASE(TT, 1, 256) GT_CASE(TT, 1, 512) GT_CASE(TT, 2, 128) GT_CASE(TT, 2, 256) \
+  GT_CASE(TT, 2, 512) GT_CASE(TT, 4, 128) GT_CASE(TT, 4, 256) GT_CASE(TT, 4, 512) GT_CASE(TT, 8, 128) \
+  GT_CASE(TT, 8, 256) GT_CASE(TT, 8, 512)
+  if (dtype == GT_F32) { GT_HCASES(float) }
+  else { GT_HCASES(__nv_bfloat16) }
+#undef GT_HCASES
+#undef GT_CASE
+  return fail(GT_ECONFIG, "unsupported (dtype, heads, heads*d)");
+}
+
 }  // namespace pipe
+
+gt_status row_stats(int dtype, int H, int D, const void* y, const void* dy, const float* lse, int64_t n, float* stats,
+                    int sb, cudaStream_t st) {
+  return pipe::row_stats_dispatch(dtype, H, D, y, dy, lse, n, stats, sb, st);
+}
 
 gt_status quantize_kv(int H, int D, const void* k, const void* v, int64_t n, void* out, int gr, int* ref,
                       cudaStream_t st) {
@@ -1880,6 +2098,7 @@ gt_status pipe_pass(gt_plan_s* P, int pass, const WorkList& w, const ChunkTable&
   a.src = es.src;
   a.win = es.win;
   a.win_bytes = es.win_bytes;
+  a.mode = es.mode;
   if (es.kv8 && pass < 2) {  // fp8 K||V table replaces the two gathered tables
     a.ga = (const char*)es.kv8;
     a.gb = nullptr;

@@ -148,6 +148,7 @@ struct gt_plan_s {
   // CSC -> CSR entry map instead of recomputing q.k and dY.v per entry
   bool es = false;
   bool es_logits = false;          // the forward's logits are part of the state (GT_ES_LOGITS, default 1)
+  bool colfirst = true;            // world-1 backward in column-first order (GT_COLFIRST=0: row-first)
   gt::DevBuf d_s2;                 // f32 [nnz_local][heads] base-2 logits of the forward, local CSR order
   gt::DevBuf d_pd;                 // (P, dS) [nnz_local][heads]: bf16x2 (bf16 plans) | f32x2, local CSR order
   gt::DevBuf d_src;                // int32 [nnz_in_local]: local CSR entry of the CSC position, -1 if remote row
@@ -298,6 +299,15 @@ gt_status launch_bwd_cols(gt_plan_s* P, const void* q, const void* k, const void
                           const void* halo_qd, const void* halo_st, void* dk, void* dv, cudaStream_t st,
                           cudaEvent_t side_ready);
 // reduce-scatter backward: partials of the halo columns summed per slot into d_rs_send (st)
+// Column-first backward (world 1, stored logits; EntryState::mode 1): cols = (LSE2, D) of every row, then
+// the column pass (dK, dV, and dS per entry in CSR order); rows = the row pass gathering k_j alone (dQ).
+gt_status launch_bwd_cf_cols(gt_plan_s* P, const void* q, const void* k, const void* v, const void* y,
+                             const float* lse, const void* dy, void* dk, void* dv, cudaStream_t st);
+gt_status launch_bwd_cf_rows(gt_plan_s* P, const void* q, const void* k, const void* v, const float* lse,
+                             const void* dy, void* dq, cudaStream_t st);
+// (LSE2, D) [n][sb bytes] of every row: LSE2 = lse log2(e), D = <dY, Y> per head
+gt_status row_stats(int dtype, int H, int D, const void* y, const void* dy, const float* lse, int64_t n,
+                    float* stats, int sb, cudaStream_t st);
 gt_status launch_bwd_halo_cols(gt_plan_s* P, const void* q, const void* dy, cudaStream_t st);
 // reduce-scatter backward: owned columns from owned rows; merged columns completed after `recv_ready`
 gt_status launch_bwd_cols_rs(gt_plan_s* P, const void* q, const void* k, const void* v, const void* dy, void* dk,
@@ -323,6 +333,10 @@ struct EntryState {
   const void* kv8 = nullptr;
   int64_t kv8_row = 0;
   const int* kvref = nullptr;
+  // 1: column-first backward (world 1, stored logits): the column pass computes dP = <dY_i, v_j> with
+  // its own v_j, P from the forward's logit (gathered through the CSC -> CSR map) and (LSE2, D) of
+  // row i, and stores dS per entry in CSR order; the row pass then gathers k_j only (launch_bwd_colfirst)
+  int mode = 0;
 };
 gt_status quantize_kv(int H, int D, const void* k, const void* v, int64_t n, void* out, int gr, int* ref,
                       cudaStream_t st);

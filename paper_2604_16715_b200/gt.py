@@ -59,7 +59,7 @@ class _Info(ctypes.Structure):
                    ("edge_state_bytes", ctypes.c_int64), ("bwd_mode", ctypes.c_int),
                    ("transport", ctypes.c_int), ("fwd_gen", ctypes.c_int64), ("stale_bwds", ctypes.c_int64),
                    ("kv_fp8", ctypes.c_int), ("kv_fp8_bytes", ctypes.c_int64), ("hot_cols", ctypes.c_int64),
-                   ("hot_entries", ctypes.c_int64)])
+                   ("hot_entries", ctypes.c_int64), ("bwd_colfirst", ctypes.c_int)])
 
 
 _lib = None

@@ -375,3 +375,34 @@ def test_host_buffer_entry_point_with_graph_replay(gt):
         assert normwise(to_f64(dk), DK) <= 2e-2 and normwise(to_f64(dv), DV) <= 2e-2, it
         check_lse(lse.numpy(), LSE, "bf16")
     plan.close()
+
+
+@pytest.mark.parametrize("h,d,dtype,heavy", [(4, 64, "bf16", 48), (8, 32, "bf16", 0), (2, 64, "f32", 40),
+                                             (8, 16, "f32", 0), (1, 128, "f32", 30)])
+def test_column_first_backward_equals_row_first(gt, h, d, dtype, heavy, monkeypatch):
+    """World-1 backward in column-first order (default: the column pass computes dP with its own v_j and
+    stores dS, the row pass gathers k_j alone) against the row-first order (GT_COLFIRST=0 at plan time):
+    the same products summed in the same trees, so dQ, dK, dV are equal bit for bit; both within tolerance
+    of the oracle."""
+    import torch
+    rp, ci = gtgen.random_graph(1500, 16000, seed=71, directed=True, power=2.0)
+    n = len(rp) - 1
+    q, k, v, dy = inputs(n, h, d, dtype, 72)
+    scale = 1.0 / math.sqrt(h * d)
+    tq, tk, tv, tdy = (to_torch(x) for x in (q, k, v, dy))
+    outs = []
+    for order in ("1", "0"):
+        monkeypatch.setenv("GT_COLFIRST", order)
+        plan = gt.Plan(rp, ci, h, d, dtype=dtype, scale=scale, heavy_threshold=heavy, edge_state=1)
+        assert plan.info()["bwd_colfirst"] == (1 if order == "1" and h * (2 if dtype == "bf16" else 4) >= 4 else 0)
+        y, lse = plan.fwd(tq, tk, tv)
+        dq, dk, dv = plan.bwd(tq, tk, tv, y, lse, tdy)
+        torch.cuda.synchronize()
+        outs.append([t.clone() for t in (dq, dk, dv)])
+        plan.close()
+    for name, a, b in zip(("dq", "dk", "dv"), outs[0], outs[1]):
+        assert torch.equal(a, b), f"{name}: column-first and row-first orders differ"
+    DQ, DK, DV, _ = oracle.backward(rp, ci, q, k, v, dy, scale)
+    for name, got, ref in zip(("dq", "dk", "dv"), outs[0], (DQ, DK, DV)):
+        e = normwise(to_f64(got), ref)
+        assert e <= TOL[dtype], f"{name}: normwise error {e:.3e} > {TOL[dtype]}"
