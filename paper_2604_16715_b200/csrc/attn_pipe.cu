@@ -811,7 +811,7 @@ struct Meta {      // warp-uniform description of one filled stage
 #define GT_MMA_BWD_MINB 5
 #endif
 #ifndef GT_CF_COLB_MINB  // column-first column pass: resident CTAs per SM (register cap)
-#define GT_CF_COLB_MINB 5
+#define GT_CF_COLB_MINB 4   // A/B: 4 (96 registers, still 5 CTAs by shared memory) vs 5 (87, rematerialised lane constants): column pass -6 %
 #endif
 template <typename T, int H, int D, int PASS, int ES>
 constexpr int min_ctas() {

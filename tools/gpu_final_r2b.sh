@@ -2,7 +2,7 @@
 # Final round-2 evidence for the committed kernels (second session): whole GPU suite, smoke, default bench
 # line, C4 / C5 bench lines with e2e and CPU baselines, ncu launch list of the default bench command,
 # ncu --set full of the three passes (refreshes the per-pass counters bench.py reads).
-O=gpurun_out/final2
+O=gpurun_out/${FINAL_DIR:-final2}
 mkdir -p $O
 python __graft_entry__.py build > $O/build.log 2>&1
 timeout 2400 python -m pytest tests -m gpu -q -s > $O/pytest_gpu_all.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu_all.log

@@ -6,7 +6,9 @@ mkdir -p gpurun_out
 python __graft_entry__.py build > gpurun_out/build.log 2>&1
 [ -z "$SKIP_TESTS" ] && { timeout 600 python -m pytest tests -m gpu -x -q -k "not fullsize" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log; }
 timeout 600 python bench.py --no-e2e --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/bench.log
-NAMES=(fwd bwd_rows bwd_cols)
+# pipe_kernel launches per step: fwd, then the backward passes in the plan's order (world 1: column pass
+# first unless GT_COLFIRST=0)
+if [ "${GT_COLFIRST:-1}" = "0" ]; then NAMES=(fwd bwd_rows bwd_cols); else NAMES=(fwd bwd_cols bwd_rows); fi
 WL=${WL:-C3-products}
 for i in ${PASSES}; do
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:pipe_kernel" -s $((3+i)) -c 1 \
