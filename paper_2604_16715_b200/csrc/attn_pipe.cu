@@ -1042,11 +1042,19 @@ __global__ void __launch_bounds__(kWarps * 32, (min_ctas<T, H, D, PASS, ES>()))
       char* dst = st + u * EB + lane * LB;
       cp_lane_z<LB>(dst, pa, valid);
       if constexpr (!(PASS == 1 && C::CF)) cp_lane_z<LB>(dst + RB, pb, valid);
-      // (LSE2, D) block of the neighbour: SB / 16 lanes copy 16 bytes each (read by all lanes of a head
-      // after the stage's wait + __syncwarp)
-      if constexpr (C::STATS) {
+      // (LSE2, D) block of the neighbour (remote-row kernels): SB / 16 lanes copy 16 bytes each (read by
+      // all lanes of a head after the stage's wait + __syncwarp)
+      if constexpr (C::STATS && HALO) {
         if (lane < C::SB / 16) cp_async16z(st + u * EB + 2 * RB + lane * 16, ps, valid);
       }
+    }
+    if constexpr (C::STATS && !HALO) {
+      // the stage's (LSE2, D) blocks in one copy: lane l < U SB/16 takes 16 bytes of neighbour l / (SB/16)
+      // (one row address per lane and stage instead of one per neighbour)
+      constexpr int LS = C::SB / 16;
+      const int su = lane / LS, sp = lane % LS;
+      const uint32_t sv = (uint32_t)__shfl_sync(kFull, win, off + su);
+      if (lane < U * LS) cp_async16z(st + su * EB + 2 * RB + sp * 16, row_addr(a.gs + sp * 16, sv, sSB), su < cnt);
     }
     }
     if constexpr ((ES & 2) && PASS == 1) {  // s2 of the stage's entries (contiguous), stored by the forward
