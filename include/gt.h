@@ -266,6 +266,11 @@ gt_status gt_attn_fwd(gt_plan_t plan, const void* q, const void* k, const void* 
  * row pass knows it before its first entry; dS_e = U_e (dP_e - D_i).  With bf16 tensors the weights
  * U_e, dS_e of the SpMM products are rounded to bf16 (the products are exact in fp32 and accumulated
  * in fp32), as the PV and dS K products of FlashAttention are (reading Z23).
+ * Order (world 1, materialised logits of this forward): column-first - a kernel writes (LSE2, D) of
+ * every row, the column pass over A^T computes dP_e = <dY_i, v_j> with its own v_j, U_e from the
+ * logit, dS_e, accumulates dK, dV and stores dS_e per entry; the row pass then gathers k_j alone for
+ * dQ (bitwise the results of the row-first order; GT_COLFIRST=0 at gt_plan selects row-first, which
+ * world > 1, the host-buffer path and backward calls of another forward always use).
  * The plan retains state of the LAST gt_attn_fwd it ran (the received K||V rows when world > 1, the
  * per-entry logits with edge_state, the head slices with GT_A2A), tagged with that forward's
  * (q, k, v, lse) pointers.  gt_attn_bwd uses the state only when its own (q, k, v, lse) are those
